@@ -1,0 +1,121 @@
+/*
+ * pastila.h -- C-ABI of the B200-native PaSTiLa hot path (libpastila.so).
+ *
+ * The reference (sniplab, /root/reference/pkg/src/sniplab) is pure Python and
+ * has no FFI of its own; this ABI is the boundary under its Python API.  Each
+ * entry point names the reference function whose semantics it provides
+ * (file:line), and the Python package paper_2401_13680_b200 binds exactly
+ * these symbols through ctypes.
+ *
+ * Conventions
+ *   - every function returns 0 on success, a negative PST_E* code on error;
+ *     pst_last_error() returns the message of the last failure on the
+ *     calling thread (ValueError-class messages reuse the reference wording);
+ *   - "host" pointers are ordinary CPU memory (pinned or pageable), "dev"
+ *     pointers are device memory of the context's GPU;
+ *   - all values are IEEE binary64, indices/labels int64;
+ *   - a context owns one GPU (one process per GPU; multi-GPU goes through
+ *     torch.distributed/NCCL above this layer).
+ */
+#ifndef PASTILA_H
+#define PASTILA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PST_OK 0
+#define PST_EINVAL -1   /* bad argument (maps to ValueError)   */
+#define PST_ECUDA -2    /* CUDA runtime failure (RuntimeError) */
+#define PST_ENOMEM -3   /* device allocation failed           */
+#define PST_ESTATE -4   /* missing prerequisite (no series)   */
+
+typedef struct pst_ctx pst_ctx;
+
+/* Snippet-search output (select_snippets, snippets.py:154-244).
+ * Caller-owned host buffers; sizes: K for the snippet arrays, N = n-m+1 for
+ * curve / nearest, K*N for profiles (row-major, in frac order), S = n/m for
+ * counts.  Any pointer may be NULL to skip that output.                    */
+typedef struct pst_snippets {
+  int64_t* indices;        /* [K] segment index, frac order               */
+  double* fracs;           /* [K]                                         */
+  double* curve;           /* [N] representativeness curve                */
+  double* profiles;        /* [K*N] chosen profiles, frac order           */
+  int64_t* counts;         /* [S] windows per nearest segment             */
+  int32_t* nearest;        /* [N] nearest segment of every window         */
+  int64_t* labels;         /* [n] per-point labels (labeling.py:91-119)   */
+  double profile_area;     /* out: sum(curve)                             */
+  double profile_max;      /* out: max over all S profiles                */
+  double criterion;        /* out: Eq. 18 score (length_select.py:56-87), 0 if K<2 */
+  int64_t unassigned;      /* out: windows whose nearest is not chosen    */
+} pst_snippets;
+
+/* ---- context --------------------------------------------------------- */
+int pst_create(int device, pst_ctx** out);
+int pst_destroy(pst_ctx* ctx);
+const char* pst_last_error(void);
+int pst_device_count(int* out);
+
+/* Upload a series and build its exact prefix sums (series.py:152-190,
+ * the sequential np.cumsum order).  Replaces TimeSeries ingestion for the
+ * device path.  x: host, n >= 2.                                          */
+int pst_set_series(pst_ctx* ctx, const double* x, int64_t n);
+/* Same from a device pointer (bench: input already resident in HBM).      */
+int pst_set_series_dev(pst_ctx* ctx, const double* x_dev, int64_t n);
+
+/* compute_sliding_stats (series.py:152-190): bit-identical to the reference
+ * on the same input.  Outputs are host arrays of n-l+1 entries (NULL ok).  */
+int pst_sliding_stats(pst_ctx* ctx, int64_t l, double* means, double* stds, double* vars);
+
+/* segment_distance_matrix / distance_row (zdist.py:138-225): distance rows
+ * for queries q0 .. q0+rows-1 against every length-l window.
+ * method 0 = sliding (correlation identity), 1 = direct z-normalization.
+ * out: host [rows * (n-l+1)].                                             */
+int pst_distance_rows(pst_ctx* ctx, int64_t l, int64_t q0, int64_t rows, int method, double* out);
+
+/* mpdist_profile / segment_profiles (mpdist.py:179-232, snippets.py:119-128):
+ * MPdist profiles of segments [seg_lo, seg_hi) at snippet size m, inner
+ * window l, order statistic k.  out: host [(seg_hi-seg_lo) * (n-m+1)].    */
+int pst_mpdist_profiles(pst_ctx* ctx, int64_t m, int64_t l, int64_t k,
+                        int64_t seg_lo, int64_t seg_hi, double* out);
+
+/* select_snippets + label_series + criterion_score for one length:
+ * all S profiles are computed on the device and never leave it; only the
+ * outputs in *res are copied back.                                        */
+int pst_select_snippets(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res);
+
+/* select_snippets(..., profiles=...) on caller-supplied host profiles
+ * D [S*N] of a series of length n (snippets.py:191-244).                  */
+int pst_select_from_profiles(pst_ctx* ctx, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
+                             pst_snippets* res);
+
+/* criterion_score (length_select.py:56-87) on host profiles P [K*N] (snippet
+ * order); out = sum over pairs of sum|P_a-P_b| / profile_max (0 if max==0). */
+int pst_criterion(pst_ctx* ctx, const double* P, int64_t K, int64_t N, double profile_max, double* out);
+/* label_series (labeling.py:91-119) on host profiles P [K*N]; labels [n].   */
+int pst_labels(pst_ctx* ctx, const double* P, int64_t K, int64_t N, int64_t n, int64_t* labels);
+
+/* ---- device-level API (multi-GPU sharding / benchmark) ----------------
+ * Profiles of segments [seg_lo, seg_hi) written to a caller-owned device
+ * matrix D_dev (row stride ld >= n-m+1).                                   */
+int pst_profiles_dev(pst_ctx* ctx, int64_t m, int64_t l, int64_t k,
+                     int64_t seg_lo, int64_t seg_hi, double* D_dev, int64_t ld);
+/* Greedy-step areas sum_j min(D[s][j], curve[j]) for rows of D_dev
+ * (curve_dev == NULL means +inf, i.e. plain row sums).  areas_dev [rows].  */
+int pst_areas_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
+                  const double* curve_dev, double* areas_dev);
+/* Per-window minimum value and first argmin over rows (ties -> lower row),
+ * row indices offset by row_base.  minval_dev [N], argmin_dev [N].        */
+int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
+                   int64_t row_base, double* minval_dev, int32_t* argmin_dev);
+/* Wait for all work queued on the context stream.                        */
+int pst_sync(pst_ctx* ctx);
+/* Kernel launches issued on the context since creation (instrumentation). */
+int64_t pst_launch_count(pst_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASTILA_H */

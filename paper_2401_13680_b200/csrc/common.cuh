@@ -1,0 +1,94 @@
+// Shared definitions for libpastila (B200 / sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/pastila.h"
+
+#define PST_INF __longlong_as_double(0x7ff0000000000000LL)
+#define FULLMASK 0xffffffffu
+
+// thread-local last error (pst_last_error)
+void pst_set_error(const char* fmt, ...);
+
+#define PST_CUDA(call)                                                         \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      pst_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e),        \
+                    __FILE__, __LINE__, cudaGetErrorString(_e));               \
+      return PST_ECUDA;                                                        \
+    }                                                                          \
+  } while (0)
+
+#define PST_TRY(expr)            \
+  do {                           \
+    int _r = (expr);             \
+    if (_r != PST_OK) return _r; \
+  } while (0)
+
+// Order-preserving 64-bit key of a NON-NEGATIVE double (callers clamp).
+__device__ __forceinline__ long long dkey(double v) { return __double_as_longlong(v); }
+__device__ __forceinline__ double kdbl(long long k) { return __longlong_as_double(k); }
+// clamp at +0 (also maps -0.0 and tiny negatives from rounding to +0.0)
+__device__ __forceinline__ double clamp0(double v) { return v > 0.0 ? v : 0.0; }
+
+// Per-length derived window data (all n-l+1 long except df/dg: n-l).
+struct LenData {
+  int64_t l = -1, Nl = 0;
+  double* mu = nullptr;     // window means (series.py:179)
+  double* var = nullptr;    // clamped variances (series.py:180-187)
+  double* sd = nullptr;     // sqrt(var)
+  double* nrm = nullptr;    // 1/sqrt(l*var), 0 for constant windows
+  double* bias = nullptr;   // e for a constant column vs non-constant query: 0.5, else 1.0
+  double* cbias = nullptr;  // e for a constant query: 0 (constant column) / 0.5
+  double* df = nullptr;     // (x[i+l]-x[i])/2
+  double* dg = nullptr;     // (x[i+l]-mc[i+1]) + (x[i]-mc[i])
+  double* mc = nullptr;     // direct window mean sum(x)/l (centering of the distance kernels)
+};
+
+struct pst_ctx {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int64_t n = 0, cap_n = 0;
+  double* x = nullptr;
+  double* csum = nullptr;   // [n+1] sequential prefix sum of x
+  double* csq = nullptr;    // [n+1] sequential prefix sum of x*x
+  int64_t* chg = nullptr;   // [n] #{t in [1,i] : x[t] != x[t-1]}
+  LenData L;
+  int64_t cap_l = 0;
+  // scratch for the MPdist tile kernel (AB matrices of in-flight tiles)
+  double* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // profile matrix D (S x N) + greedy buffers
+  double* D = nullptr;
+  size_t D_bytes = 0;
+  void* work = nullptr;
+  size_t work_bytes = 0;
+  int64_t launches = 0;
+  double* dbg = nullptr;
+  size_t dbg_bytes = 0;
+  int64_t dbg_T = 0, dbg_NC = 0, dbg_w = 0;
+  int num_sms = 148;
+  size_t smem_optin = 0;
+};
+
+int pst_ensure(void** p, size_t* cap, size_t bytes);
+int pst_ensure_len(pst_ctx* c, int64_t l);
+
+// kernels launched from several translation units
+struct MPArgs {
+  const double *x, *mu /* centering means (LenData::mc) */, *nrm, *bias, *cbias, *df, *dg;
+  int64_t n, l, m, w, k, Nl, N, T;
+  int64_t seg0;      // segment of blockIdx.y == 0
+  double* D;         // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y)
+  int64_t ldD, rowD0;
+  double* ab;        // scratch, w*T doubles per CTA
+  double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
+};
+
+int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                  double* D_dev, int64_t ld);

@@ -1,0 +1,868 @@
+// libpastila: context, sliding statistics, distance rows, greedy snippet
+// selection, nearest-segment attribution, labels, Eq. 18 criterion, C-ABI.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <numeric>
+#include <vector>
+
+static thread_local std::string g_err;
+
+void pst_set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+int pst_ensure(void** p, size_t* cap, size_t bytes) {
+  if (bytes <= *cap && *p) return PST_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  if (bytes == 0) return PST_OK;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    pst_set_error("device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    *p = nullptr;
+    return PST_ENOMEM;
+  }
+  *cap = bytes;
+  return PST_OK;
+}
+
+namespace {
+
+// ----------------------------------------------------------------- kernels
+// Exact sequential prefix sums (np.cumsum order, series.py:177-178) and the
+// running count of value changes (constant-window test, series.py:183-187).
+__global__ void k_prefix(const double* __restrict__ x, int64_t n, double* csum, double* csq, int64_t* chg) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0, q = 0.0;
+  int64_t c = 0;
+  csum[0] = 0.0;
+  csq[0] = 0.0;
+  double prev = x[0];
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = x[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s = __dadd_rn(s, v[u]);
+      q = __dadd_rn(q, __dmul_rn(v[u], v[u]));
+      if (i + u > 0 && v[u] != prev) ++c;
+      prev = v[u];
+      csum[i + u + 1] = s;
+      csq[i + u + 1] = q;
+      chg[i + u] = c;
+    }
+  }
+  for (; i < n; ++i) {
+    const double v = x[i];
+    s = __dadd_rn(s, v);
+    q = __dadd_rn(q, __dmul_rn(v, v));
+    if (i > 0 && v != prev) ++c;
+    prev = v;
+    csum[i + 1] = s;
+    csq[i + 1] = q;
+    chg[i] = c;
+  }
+}
+
+__device__ __forceinline__ double win_mean(const double* csum, int64_t i, int64_t l) {
+  return __ddiv_rn(__dsub_rn(csum[i + l], csum[i]), (double)l);
+}
+
+// Per-length window statistics, bit-identical to series.py:179-189, plus the
+// derived arrays of the distance recurrence (see mpdist.cu header).
+__global__ void k_stats(const double* __restrict__ x, const double* __restrict__ csum,
+                        const double* __restrict__ csq, const int64_t* __restrict__ chg, int64_t n,
+                        int64_t l, LenData L) {
+  const int64_t Nl = n - l + 1;
+  const double dl = (double)l;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Nl; i += (int64_t)gridDim.x * blockDim.x) {
+    const double mu = win_mean(csum, i, l);
+    double v = __dsub_rn(__ddiv_rn(__dsub_rn(csq[i + l], csq[i]), dl), __dmul_rn(mu, mu));
+    v = v > 0.0 ? v : 0.0;                        // np.maximum(var, 0)
+    if (chg[i + l - 1] - chg[i] == 0) v = 0.0;    // sliding max == sliding min
+    L.mu[i] = mu;
+    L.var[i] = v;
+    L.sd[i] = __dsqrt_rn(v);
+    const bool cst = (v == 0.0);
+    // Distance kernels center with the direct window mean and normalize with the
+    // centered sum of squares (two-pass): accurate even where the prefix-sum
+    // variance cancels.  The constant flag keeps the reference rule above.
+    double sx = 0.0;
+    for (int64_t t = 0; t < l; ++t) sx += x[i + t];
+    const double mc = sx / dl;
+    L.mc[i] = mc;
+    double css = 0.0;
+    if (!cst)
+      for (int64_t t = 0; t < l; ++t) {
+        const double d = x[i + t] - mc;
+        css = fma(d, d, css);
+      }
+    L.nrm[i] = (cst || css <= 0.0) ? 0.0 : __drcp_rn(__dsqrt_rn(css));
+    L.bias[i] = cst ? 0.5 : 1.0;
+    L.cbias[i] = cst ? 0.0 : 0.5;
+
+  }
+}
+
+__global__ void k_dfdg(const double* __restrict__ x, int64_t n, int64_t l, LenData L) {
+  const int64_t Nl = n - l + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < Nl; i += (int64_t)gridDim.x * blockDim.x) {
+    L.df[i] = (x[i + l] - x[i]) * 0.5;
+    L.dg[i] = (x[i + l] - L.mc[i + 1]) + (x[i] - L.mc[i]);
+  }
+}
+
+// Distance rows for queries q0..q0+rows-1 (zdist.py:191-225): one thread per
+// diagonal; diagonals entering at row 0 (column c0 >= 0) or at column 0
+// (row r0 > 0) start from a fresh centered dot product.
+__global__ void k_rows(const double* __restrict__ x, LenData L, int64_t n, int64_t l, int64_t q0,
+                       int64_t rows, double* __restrict__ out) {
+  const int64_t Nl = n - l + 1;
+  const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - (rows - 1);  // column - row
+  if (d >= Nl) return;
+  int64_t r = d >= 0 ? 0 : -d;
+  int64_t c = d >= 0 ? d : 0;
+  if (r >= rows) return;
+  int64_t q = q0 + r;
+  double cov = 0.0;
+  {
+    const double mq = L.mc[q], mc = L.mc[c];
+    double acc = 0.0, sq = 0.0;
+    for (int64_t t = 0; t < l; ++t) {
+      const double xq = x[q + t] - mq;
+      acc = fma(xq, x[c + t], acc);
+      sq += xq;
+    }
+    cov = fma(-mc, sq, acc);
+  }
+  const double twol = 2.0 * (double)l;
+  for (;;) {
+    double e;
+    const double nq = L.nrm[q];
+    if (nq == 0.0)
+      e = L.cbias[c];
+    else
+      e = fma(-(cov * nq), L.nrm[c], L.bias[c]);
+    if (c == q) e = 0.0;
+    e = clamp0(e);
+    if (e < 1e-15) e = 0.0;
+    if (e > 2.0) e = 2.0;
+    out[r * Nl + c] = sqrt(twol * e);
+    if (++r >= rows || c + 1 >= Nl) break;
+    cov = fma(L.df[q], L.dg[c], fma(L.dg[q], L.df[c], cov));
+    ++q;
+    ++c;
+  }
+}
+
+// Direct z-normalized distances (zdist.py:126-135): explicit per-window
+// mean/std (two-pass), constant windows z-normalize to zeros.
+__global__ void k_rows_direct(const double* __restrict__ x, int64_t n, int64_t l, int64_t q0, int64_t rows,
+                              double* __restrict__ out) {
+  const int64_t Nl = n - l + 1;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = blockIdx.y;
+  if (c >= Nl || r >= rows) return;
+  const int64_t q = q0 + r;
+  auto stat = [&](int64_t s0, double& mean, double& sdv, bool& flat) {
+    double s = 0.0, mn = x[s0], mx = x[s0];
+    for (int64_t t = 0; t < l; ++t) {
+      s += x[s0 + t];
+      mn = fmin(mn, x[s0 + t]);
+      mx = fmax(mx, x[s0 + t]);
+    }
+    mean = s / (double)l;
+    double ss = 0.0;
+    for (int64_t t = 0; t < l; ++t) {
+      const double dv = x[s0 + t] - mean;
+      ss += dv * dv;
+    }
+    sdv = sqrt(ss / (double)l);
+    flat = (mn == mx) || sdv == 0.0;
+  };
+  double mq, sq, mc, sc;
+  bool fq, fc;
+  stat(q, mq, sq, fq);
+  stat(c, mc, sc, fc);
+  double acc = 0.0;
+  for (int64_t t = 0; t < l; ++t) {
+    const double zq = fq ? 0.0 : (x[q + t] - mq) / sq;
+    const double zc = fc ? 0.0 : (x[c + t] - mc) / sc;
+    acc += (zq - zc) * (zq - zc);
+  }
+  out[r * Nl + c] = (c == q) ? 0.0 : sqrt(acc);
+}
+
+// Deterministic block reduction helpers (fixed order: per-thread strided
+// sequential sum, then a fixed shuffle tree) -- identical rows give
+// bit-identical sums, as numpy row sums do (snippets.py:205).
+template <int NT>
+__device__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int wv = 0; wv < NT / 32; ++wv) t += sh[wv];
+  __syncthreads();
+  return t;
+}
+
+// areas[r] = sum_j min(D[r][j], curve[j])  (curve == nullptr: +inf)
+__global__ void __launch_bounds__(256) k_areas(const double* __restrict__ D, int64_t N, int64_t ld,
+                                               const double* __restrict__ curve, double* areas) {
+  __shared__ double sh[8];
+  const double* row = D + blockIdx.x * ld;
+  double acc = 0.0;
+  if (curve) {
+    for (int64_t j = threadIdx.x; j < N; j += 256) acc += fmin(row[j], curve[j]);
+  } else {
+    for (int64_t j = threadIdx.x; j < N; j += 256) acc += row[j];
+  }
+  const double t = block_sum<256>(acc, sh);
+  if (threadIdx.x == 0) areas[blockIdx.x] = t;
+}
+
+// argmin over available rows (ties -> lowest index, snippets.py:207); marks it taken,
+// folds it into the curve in a follow-up kernel.
+__global__ void __launch_bounds__(1024) k_pick(const double* __restrict__ areas, uint8_t* taken, int64_t S,
+                                               int64_t* best_out) {
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  double v = PST_INF;
+  int64_t idx = INT64_MAX;
+  for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
+    if (taken[s]) continue;
+    const double a = areas[s];
+    if (a < v || (a == v && s < idx)) {
+      v = a;
+      idx = s;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(FULLMASK, v, o);
+    const int64_t oi = __shfl_xor_sync(FULLMASK, idx, o);
+    if (ov < v || (ov == v && oi < idx)) {
+      v = ov;
+      idx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    bv[threadIdx.x >> 5] = v;
+    bi[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int wv = 1; wv < (int)(blockDim.x >> 5); ++wv)
+      if (bv[wv] < v || (bv[wv] == v && bi[wv] < idx)) {
+        v = bv[wv];
+        idx = bi[wv];
+      }
+    if (idx == INT64_MAX) {  // all taken or all +inf areas: lowest available index
+      for (int64_t s = 0; s < S; ++s)
+        if (!taken[s]) {
+          idx = s;
+          break;
+        }
+    }
+    *best_out = idx;
+    taken[idx] = 1;
+  }
+}
+
+__global__ void k_curve(double* curve, const double* __restrict__ D, int64_t ld, const int64_t* best, int64_t N) {
+  const double* row = D + (*best) * ld;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    curve[j] = fmin(curve[j], row[j]);
+}
+
+__global__ void k_fill(double* p, double v, int64_t N) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) p[j] = v;
+}
+
+// Per-window first argmin over rows (snippets.py:212, labeling.py:115).
+__global__ void k_colmin(const double* __restrict__ D, int64_t rows, int64_t N, int64_t ld, int64_t base,
+                         double* minval, int32_t* arg) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    double b = D[j];
+    int64_t bi = 0;
+    for (int64_t r = 1; r < rows; ++r) {
+      const double v = D[r * ld + j];
+      if (v < b) {
+        b = v;
+        bi = r;
+      }
+    }
+    if (minval) minval[j] = b;
+    arg[j] = (int32_t)(bi + base);
+  }
+}
+
+__global__ void k_count(const int32_t* __restrict__ arg, int64_t N, unsigned long long* counts) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&counts[arg[j]], 1ull);
+}
+
+// max over the S x N matrix (profile_max, snippets.py:241): order independent.
+__global__ void k_max(const double* __restrict__ D, int64_t rows, int64_t N, int64_t ld, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+      m = fmax(m, D[r * ld + j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULLMASK, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// Eq. 18 pair sums: sum_j |P_a[j] - P_b[j]| for one (a, b) pair per CTA.
+__global__ void __launch_bounds__(256) k_pairdiff(const double* __restrict__ P, int64_t N, int64_t K,
+                                                  double* out) {
+  __shared__ double sh[8];
+  int64_t a = 0, b = 0, t = blockIdx.x;
+  for (a = 0; a < K; ++a) {
+    const int64_t cnt = K - 1 - a;
+    if (t < cnt) {
+      b = a + 1 + t;
+      break;
+    }
+    t -= cnt;
+  }
+  const double* pa = P + a * N;
+  const double* pb = P + b * N;
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < N; j += 256) acc += fabs(pa[j] - pb[j]);
+  const double s = block_sum<256>(acc, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// labels (labeling.py:114-118): argmin over K ordered profiles, tail copies the last window.
+__global__ void k_labels(const double* __restrict__ P, int64_t K, int64_t N, int64_t n, int64_t* labels) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i < N ? i : N - 1;
+    double b = P[j];
+    int64_t bi = 0;
+    for (int64_t r = 1; r < K; ++r) {
+      const double v = P[r * N + j];
+      if (v < b) {
+        b = v;
+        bi = r;
+      }
+    }
+    labels[i] = bi;
+  }
+}
+
+__global__ void k_gather_rows(const double* __restrict__ D, int64_t ld, const int64_t* __restrict__ idx, int64_t K,
+                              int64_t N, double* out) {
+  const int64_t r = blockIdx.y;
+  const double* row = D + idx[r] * ld;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    out[r * N + j] = row[j];
+}
+
+int grid_for(int64_t n, int threads, int cap = 148 * 16) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+bool valid(pst_ctx* c) {
+  if (!c) {
+    pst_set_error("null context");
+    return false;
+  }
+  return true;
+}
+
+int need_series(pst_ctx* c) {
+  if (c->n <= 0) {
+    pst_set_error("no series uploaded (call pst_set_series first)");
+    return PST_ESTATE;
+  }
+  return PST_OK;
+}
+
+}  // namespace
+
+int pst_ensure_len(pst_ctx* c, int64_t l) {
+  PST_TRY(need_series(c));
+  if (l < 1 || l > c->n) {
+    pst_set_error("window length %lld out of range [1, %lld]", (long long)l, (long long)c->n);
+    return PST_EINVAL;
+  }
+  if (c->L.l == l) return PST_OK;
+  const int64_t Nl = c->n - l + 1;
+  if (Nl > c->cap_l) {
+    double** arrs[] = {&c->L.mu, &c->L.var, &c->L.sd, &c->L.nrm, &c->L.bias, &c->L.cbias, &c->L.df, &c->L.dg, &c->L.mc};
+    for (double** a : arrs) {
+      if (*a) cudaFree(*a);
+      *a = nullptr;
+      cudaError_t e = cudaMalloc((void**)a, (size_t)(Nl + 1) * sizeof(double));
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        pst_set_error("device allocation for window statistics failed: %s", cudaGetErrorString(e));
+        c->cap_l = 0;
+        c->L.l = -1;
+        return PST_ENOMEM;
+      }
+    }
+    c->cap_l = Nl;
+  }
+  k_stats<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->csum, c->csq, c->chg, c->n, l, c->L);
+  k_dfdg<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->n, l, c->L);
+  c->launches += 2;
+  PST_CUDA(cudaGetLastError());
+  c->L.l = l;
+  c->L.Nl = Nl;
+  return PST_OK;
+}
+
+// ================================================================== C-ABI
+extern "C" {
+
+const char* pst_last_error(void) { return g_err.c_str(); }
+
+int pst_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out = 0;
+    pst_set_error("cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    return PST_ECUDA;
+  }
+  *out = n;
+  return PST_OK;
+}
+
+int pst_create(int device, pst_ctx** out) {
+  *out = nullptr;
+  int nd = 0;
+  PST_TRY(pst_device_count(&nd));
+  if (device < 0 || device >= nd) {
+    pst_set_error("device %d out of range [0, %d)", device, nd);
+    return PST_EINVAL;
+  }
+  PST_CUDA(cudaSetDevice(device));
+  pst_ctx* c = new pst_ctx();
+  c->dev = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    pst_set_error("cudaStreamCreate: %s", cudaGetErrorString(e));
+    return PST_ECUDA;
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  c->smem_optin = (size_t)optin;
+  *out = c;
+  return PST_OK;
+}
+
+int pst_destroy(pst_ctx* c) {
+  if (!c) return PST_OK;
+  cudaSetDevice(c->dev);
+  cudaStreamSynchronize(c->st);
+  void* ptrs[] = {c->x, c->csum, c->csq, c->chg, c->L.mu, c->L.var, c->L.sd, c->L.nrm, c->L.bias,
+                  c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  cudaStreamDestroy(c->st);
+  delete c;
+  return PST_OK;
+}
+
+static int set_series_common(pst_ctx* c, const double* x, int64_t n, cudaMemcpyKind kind) {
+  if (!valid(c)) return PST_EINVAL;
+  if (n < 2) {
+    pst_set_error("series needs at least 2 samples, got %lld", (long long)n);
+    return PST_EINVAL;
+  }
+  PST_CUDA(cudaSetDevice(c->dev));
+  if (n > c->cap_n) {
+    void** arrs[] = {(void**)&c->x, (void**)&c->csum, (void**)&c->csq, (void**)&c->chg};
+    for (void** a : arrs) {
+      if (*a) cudaFree(*a);
+      *a = nullptr;
+    }
+    c->cap_n = 0;
+    size_t cap = 0;
+    PST_TRY(pst_ensure((void**)&c->x, &cap, (size_t)n * sizeof(double)));
+    cap = 0;
+    PST_TRY(pst_ensure((void**)&c->csum, &cap, (size_t)(n + 1) * sizeof(double)));
+    cap = 0;
+    PST_TRY(pst_ensure((void**)&c->csq, &cap, (size_t)(n + 1) * sizeof(double)));
+    cap = 0;
+    PST_TRY(pst_ensure((void**)&c->chg, &cap, (size_t)(n + 1) * sizeof(int64_t)));
+    c->cap_n = n;
+  }
+  PST_CUDA(cudaMemcpyAsync(c->x, x, (size_t)n * sizeof(double), kind, c->st));
+  c->n = n;
+  c->L.l = -1;
+  k_prefix<<<1, 32, 0, c->st>>>(c->x, n, c->csum, c->csq, c->chg);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+int pst_set_series(pst_ctx* c, const double* x, int64_t n) {
+  return set_series_common(c, x, n, cudaMemcpyHostToDevice);
+}
+
+int pst_set_series_dev(pst_ctx* c, const double* x, int64_t n) {
+  return set_series_common(c, x, n, cudaMemcpyDeviceToDevice);
+}
+
+int pst_sync(pst_ctx* c) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+int64_t pst_launch_count(pst_ctx* c) { return c ? c->launches : -1; }
+
+int pst_sliding_stats(pst_ctx* c, int64_t l, double* means, double* stds, double* vars) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(pst_ensure_len(c, l));
+  const size_t b = (size_t)c->L.Nl * sizeof(double);
+  if (means) PST_CUDA(cudaMemcpyAsync(means, c->L.mu, b, cudaMemcpyDeviceToHost, c->st));
+  if (stds) PST_CUDA(cudaMemcpyAsync(stds, c->L.sd, b, cudaMemcpyDeviceToHost, c->st));
+  if (vars) PST_CUDA(cudaMemcpyAsync(vars, c->L.var, b, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+int pst_distance_rows(pst_ctx* c, int64_t l, int64_t q0, int64_t rows, int method, double* out) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(pst_ensure_len(c, l));
+  const int64_t Nl = c->n - l + 1;
+  if (rows < 1 || q0 < 0 || q0 + rows > Nl) {
+    pst_set_error("query window [%lld, %lld) is outside a series of length %lld", (long long)(q0 + rows - 1),
+                  (long long)(q0 + rows - 1 + l), (long long)c->n);
+    return PST_EINVAL;
+  }
+  const size_t bytes = (size_t)rows * Nl * sizeof(double);
+  PST_TRY(pst_ensure(&c->work, &c->work_bytes, bytes));
+  double* d = (double*)c->work;
+  if (method == 0) {
+    const int64_t nd = Nl + rows - 1;
+    k_rows<<<(unsigned)((nd + 255) / 256), 256, 0, c->st>>>(c->x, c->L, c->n, l, q0, rows, d);
+  } else if (method == 1) {
+    dim3 g((unsigned)((Nl + 255) / 256), (unsigned)rows);
+    k_rows_direct<<<g, 256, 0, c->st>>>(c->x, c->n, l, q0, rows, d);
+  } else {
+    pst_set_error("unknown method %d, expected 0 (sliding) or 1 (direct)", method);
+    return PST_EINVAL;
+  }
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  PST_CUDA(cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+static int check_mkl(pst_ctx* c, int64_t m, int64_t l, int64_t k) {
+  PST_TRY(need_series(c));
+  if (m < 2) {
+    pst_set_error("snippet size must be at least 2, got %lld", (long long)m);
+    return PST_EINVAL;
+  }
+  if (m > c->n) {
+    pst_set_error("snippet size %lld exceeds series length %lld", (long long)m, (long long)c->n);
+    return PST_EINVAL;
+  }
+  if (l < 1 || l > m) {
+    pst_set_error("window size %lld out of range [1, %lld]", (long long)l, (long long)m);
+    return PST_EINVAL;
+  }
+  if (k < 1) {
+    pst_set_error("order statistic must be at least 1, got %lld", (long long)k);
+    return PST_EINVAL;
+  }
+  return PST_OK;
+}
+
+int pst_profiles_dev(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, double* D_dev,
+                     int64_t ld) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t S = c->n / m;
+  if (seg_lo < 0 || seg_hi > S || seg_lo >= seg_hi) {
+    pst_set_error("segment index %lld out of range [0, %lld)", (long long)(seg_lo < 0 ? seg_lo : seg_hi - 1),
+                  (long long)S);
+    return PST_EINVAL;
+  }
+  if (ld < c->n - m + 1) {
+    pst_set_error("row stride %lld smaller than the window count %lld", (long long)ld, (long long)(c->n - m + 1));
+    return PST_EINVAL;
+  }
+  return launch_mpdist(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+}
+
+int pst_mpdist_profiles(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, double* out) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t N = c->n - m + 1;
+  const size_t bytes = (size_t)(seg_hi - seg_lo) * N * sizeof(double);
+  PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, bytes > 0 ? bytes : 8));
+  PST_TRY(pst_profiles_dev(c, m, l, k, seg_lo, seg_hi, c->D, N));
+  PST_CUDA(cudaMemcpyAsync(out, c->D, bytes, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+int pst_areas_dev(pst_ctx* c, const double* D, int64_t rows, int64_t N, int64_t ld, const double* curve,
+                  double* areas) {
+  if (!valid(c)) return PST_EINVAL;
+  if (rows <= 0) return PST_OK;
+  k_areas<<<(unsigned)rows, 256, 0, c->st>>>(D, N, ld, curve, areas);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+int pst_colmin_dev(pst_ctx* c, const double* D, int64_t rows, int64_t N, int64_t ld, int64_t base, double* minval,
+                   int32_t* arg) {
+  if (!valid(c)) return PST_EINVAL;
+  if (rows <= 0) return PST_OK;
+  k_colmin<<<grid_for(N, 256), 256, 0, c->st>>>(D, rows, N, ld, base, minval, arg);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
+                      pst_snippets* res);
+
+int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t n = c->n, S = n / m, N = n - m + 1;
+  if (S < 2) {
+    pst_set_error("snippet size %lld leaves only %lld segment(s) of a series of length %lld; need at least 2",
+                  (long long)m, (long long)S, (long long)n);
+    return PST_EINVAL;
+  }
+  if (K < 1 || K > S) {
+    pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
+    return PST_EINVAL;
+  }
+  PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)S * N * sizeof(double)));
+  PST_TRY(launch_mpdist(c, m, l, k, 0, S, c->D, N));
+  return run_select(c, c->D, S, N, n, K, res);
+}
+
+// select_snippets(..., profiles=...) (snippets.py:191-196): greedy + attribution on
+// caller-supplied host profiles D [S*N].
+int pst_select_from_profiles(pst_ctx* c, const double* Dh, int64_t S, int64_t N, int64_t n, int64_t K,
+                             pst_snippets* res) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  if (S < 1 || N < 1 || n < N || K < 1 || K > S) {
+    pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
+    return PST_EINVAL;
+  }
+  PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)S * N * sizeof(double)));
+  PST_CUDA(cudaMemcpyAsync(c->D, Dh, (size_t)S * N * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  return run_select(c, c->D, S, N, n, K, res);
+}
+
+static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
+                      pst_snippets* res) {
+  // device buffers: D (S x N), work: curve[N], areas[S], taken[S], best[K], counts[S], nearest[N],
+  // ordered profiles [K x N], labels[n], pair sums, max
+  const int64_t npair = K * (K - 1) / 2;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_curve = take(N * 8), o_areas = take(S * 8), o_taken = take(S), o_best = take(K * 8),
+               o_counts = take(S * 8), o_near = take(N * 4), o_prof = take(K * N * 8), o_lab = take(n * 8),
+               o_pair = take((npair + 1) * 8), o_max = take(8), o_ord = take(K * 8);
+  PST_TRY(pst_ensure(&c->work, &c->work_bytes, off));
+  char* wb = (char*)c->work;
+  double* curve = (double*)(wb + o_curve);
+  double* areas = (double*)(wb + o_areas);
+  uint8_t* taken = (uint8_t*)(wb + o_taken);
+  int64_t* best = (int64_t*)(wb + o_best);
+  unsigned long long* counts = (unsigned long long*)(wb + o_counts);
+  int32_t* nearest = (int32_t*)(wb + o_near);
+  double* prof = (double*)(wb + o_prof);
+  int64_t* labels = (int64_t*)(wb + o_lab);
+  double* pair = (double*)(wb + o_pair);
+  unsigned long long* dmax = (unsigned long long*)(wb + o_max);
+  int64_t* ord = (int64_t*)(wb + o_ord);
+
+  // profile_max
+  PST_CUDA(cudaMemsetAsync(dmax, 0, 8, c->st));
+  {
+    dim3 g((unsigned)grid_for(N, 256, 64), (unsigned)std::min<int64_t>(S, 64));
+    k_max<<<g, 256, 0, c->st>>>(D, S, N, N, dmax);
+    c->launches++;
+  }
+  // greedy (snippets.py:201-210)
+  PST_CUDA(cudaMemsetAsync(taken, 0, S, c->st));
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(curve, HUGE_VAL, N);
+  c->launches++;
+  for (int64_t step = 0; step < K; ++step) {
+    k_areas<<<(unsigned)S, 256, 0, c->st>>>(D, N, N, step == 0 ? nullptr : curve, areas);
+    k_pick<<<1, 1024, 0, c->st>>>(areas, taken, S, best + step);
+    k_curve<<<grid_for(N, 256), 256, 0, c->st>>>(curve, D, N, best + step, N);
+    c->launches += 3;
+  }
+  PST_CUDA(cudaGetLastError());
+  // attribution (snippets.py:212-213)
+  PST_CUDA(cudaMemsetAsync(counts, 0, S * 8, c->st));
+  k_colmin<<<grid_for(N, 256), 256, 0, c->st>>>(D, S, N, N, 0, nullptr, nearest);
+  k_count<<<grid_for(N, 256), 256, 0, c->st>>>(nearest, N, counts);
+  c->launches += 2;
+  PST_CUDA(cudaGetLastError());
+  // host: chosen order by (-frac, index)  (snippets.py:228)
+  std::vector<int64_t> chosen(K);
+  std::vector<unsigned long long> hcounts(S);
+  unsigned long long hmax = 0;
+  PST_CUDA(cudaMemcpyAsync(chosen.data(), best, K * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(hcounts.data(), counts, S * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  std::vector<int64_t> order(K);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    const double fa = (double)hcounts[chosen[a]] / (double)N, fb = (double)hcounts[chosen[b]] / (double)N;
+    if (fa != fb) return fa > fb;
+    return chosen[a] < chosen[b];
+  });
+  std::vector<int64_t> ordidx(K);
+  for (int64_t r = 0; r < K; ++r) ordidx[r] = chosen[order[r]];
+  PST_CUDA(cudaMemcpyAsync(ord, ordidx.data(), K * 8, cudaMemcpyHostToDevice, c->st));
+  {
+    dim3 g((unsigned)grid_for(N, 256, 256), (unsigned)K);
+    k_gather_rows<<<g, 256, 0, c->st>>>(D, N, ord, K, N, prof);
+    c->launches++;
+  }
+  if (res->labels) {
+    k_labels<<<grid_for(n, 256), 256, 0, c->st>>>(prof, K, N, n, labels);
+    c->launches++;
+  }
+  if (npair > 0) {
+    k_pairdiff<<<(unsigned)npair, 256, 0, c->st>>>(prof, N, K, pair);
+    c->launches++;
+  }
+  // curve area: deterministic device sum
+  k_areas<<<1, 256, 0, c->st>>>(curve, N, N, nullptr, areas);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  double area = 0.0;
+  std::vector<double> hpair(npair > 0 ? npair : 1);
+  PST_CUDA(cudaMemcpyAsync(&area, areas, 8, cudaMemcpyDeviceToHost, c->st));
+  if (npair > 0) PST_CUDA(cudaMemcpyAsync(hpair.data(), pair, npair * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->curve) PST_CUDA(cudaMemcpyAsync(res->curve, curve, N * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->profiles) PST_CUDA(cudaMemcpyAsync(res->profiles, prof, K * N * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->nearest) PST_CUDA(cudaMemcpyAsync(res->nearest, nearest, N * 4, cudaMemcpyDeviceToHost, c->st));
+  if (res->labels) PST_CUDA(cudaMemcpyAsync(res->labels, labels, n * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  res->profile_area = area;
+  double pm;
+  memcpy(&pm, &hmax, 8);
+  res->profile_max = pm;
+  double tot = 0.0;
+  for (int64_t p = 0; p < npair; ++p) tot += hpair[p];  // itertools.combinations order
+  res->criterion = (K < 2 || pm == 0.0) ? 0.0 : tot / pm;
+  int64_t covered = 0;
+  for (int64_t r = 0; r < K; ++r) {
+    if (res->indices) res->indices[r] = ordidx[r];
+    if (res->fracs) res->fracs[r] = (double)hcounts[ordidx[r]] / (double)N;
+    covered += (int64_t)hcounts[ordidx[r]];
+  }
+  if (res->counts)
+    for (int64_t s = 0; s < S; ++s) res->counts[s] = (int64_t)hcounts[s];
+  res->unassigned = N - covered;
+  return PST_OK;
+}
+
+// criterion_score on caller-supplied profiles (length_select.py:56-87):
+// P host [K*N] in snippet order, pairs summed in itertools.combinations order.
+int pst_criterion(pst_ctx* c, const double* P, int64_t K, int64_t N, double profile_max, double* out) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  if (K < 2) {
+    pst_set_error("separation needs at least 2 snippets, got %lld", (long long)K);
+    return PST_EINVAL;
+  }
+  if (profile_max == 0.0) {
+    *out = 0.0;
+    return PST_OK;
+  }
+  const int64_t npair = K * (K - 1) / 2;
+  const size_t bp = (size_t)K * N * 8;
+  PST_TRY(pst_ensure(&c->work, &c->work_bytes, bp + npair * 8 + 256));
+  double* dP = (double*)c->work;
+  double* dpair = (double*)((char*)c->work + ((bp + 255) & ~(size_t)255));
+  PST_CUDA(cudaMemcpyAsync(dP, P, bp, cudaMemcpyHostToDevice, c->st));
+  k_pairdiff<<<(unsigned)npair, 256, 0, c->st>>>(dP, N, K, dpair);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  std::vector<double> h(npair);
+  PST_CUDA(cudaMemcpyAsync(h.data(), dpair, npair * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  double tot = 0.0;
+  for (int64_t i = 0; i < npair; ++i) tot += h[i];
+  *out = tot / profile_max;
+  return PST_OK;
+}
+
+// label_series on caller-supplied ordered profiles (labeling.py:91-119).
+int pst_labels(pst_ctx* c, const double* P, int64_t K, int64_t N, int64_t n, int64_t* labels) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  if (K < 1 || N < 1 || n < N) {
+    pst_set_error("bad label shapes K=%lld N=%lld n=%lld", (long long)K, (long long)N, (long long)n);
+    return PST_EINVAL;
+  }
+  const size_t bp = ((size_t)K * N * 8 + 255) & ~(size_t)255;
+  PST_TRY(pst_ensure(&c->work, &c->work_bytes, bp + (size_t)n * 8));
+  double* dP = (double*)c->work;
+  int64_t* dl = (int64_t*)((char*)c->work + bp);
+  PST_CUDA(cudaMemcpyAsync(dP, P, (size_t)K * N * 8, cudaMemcpyHostToDevice, c->st));
+  k_labels<<<grid_for(n, 256), 256, 0, c->st>>>(dP, K, N, n, dl);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  PST_CUDA(cudaMemcpyAsync(labels, dl, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// debug: AB matrix (w x T) and allP_BA (NC) of the first tile of the last profile launch
+int pst_debug_last_tile(pst_ctx* c, double* ab, double* ba, int64_t* dims) {
+  if (!c->dbg) { pst_set_error("PASTILA_DEBUG not set"); return PST_ESTATE; }
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  dims[0] = c->dbg_w; dims[1] = c->dbg_T; dims[2] = c->dbg_NC;
+  if (ab) PST_CUDA(cudaMemcpy(ab, c->scratch, (size_t)c->dbg_w * c->dbg_T * 8, cudaMemcpyDeviceToHost));
+  if (ba) PST_CUDA(cudaMemcpy(ba, c->dbg, (size_t)c->dbg_NC * 8, cudaMemcpyDeviceToHost));
+  return PST_OK;
+}
+
+}  // extern "C"

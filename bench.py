@@ -1,0 +1,334 @@
+"""Benchmark: PaSTiLa length sweep at n=1M (BASELINE.json config 3) on B200.
+
+One "step" = one full snippet-length sweep over the C3 workload: synthetic
+planted walk (n=1,000,000, A=4 activities, m_act=256, seed 0),
+m in {64, 96, ..., 512} (15 lengths), K=4 snippets, l=ceil(m/2), k=ceil(m/10):
+all S=n//m MPdist profiles per length, greedy pick, attribution, Eq. 18
+criterion, labels, and the argmax length.  Unit of work = one subsequence
+pair (ED_matr entry, Eq. 9): S*w*N_l per length (the reference's
+default_cost, scheduler.py:90-102).  Metric: pairs/s (whole job).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pastila|reference]
+
+N>1: launched by torchrun (one process per GPU); lengths are sharded by
+Karmarkar-Karp over ranks (weak... strong scaling: the total work is fixed).
+Timing: barrier + synchronize, CUDA events on the library stream, max over
+ranks.  Inputs (8 MB) are far smaller than L2 and are re-derived inside the
+step (prefix sums recomputed), and each length's working set (S*N profile
+matrix, 15-125 GB) is far larger than L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_SERIES = 1_000_000
+GRID = list(range(64, 513, 32))
+K_SNIPPETS = 4
+M_ACT, N_ACT, SEED = 256, 4, 0
+FP64_FLOPS_PER_PAIR = 8  # 2 FMA QT update + 1 FMA + 2 MUL correlation
+METRIC = "end-to-end PaSTiLa time (s) and subsequence-pairs/sec at n=1M, 1/2/4/8 B200"
+
+
+def pairs_of(n: int, m: int) -> int:
+    l = -(-m // 2)
+    return (m - l + 1) * (n - l + 1) * (n // m)
+
+
+def workload():
+    from paper_2401_13680_b200.datagen import planted_walk
+
+    x, _ = planted_walk(N_SERIES, m_act=M_ACT, A=N_ACT, seed=SEED)
+    return x
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 1, 0, 0
+    import torch
+    import torch.distributed as dist
+
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ["PASTILA_DEVICE"] = str(lr)
+    torch.cuda.set_device(lr)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+    return ws, dist.get_rank(), lr
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                f = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(f) == 6:
+                    self.samples.append(f)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def fp64_peak():
+    p = ROOT / "profiles" / "r01_fp64_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["fp64_fma_tflops"]), "measured (profiles/r01_fp64_peak.json, tools/fpeak.cu)"
+    return 37.0, "datasheet"
+
+
+def cpu_sample_pairs_per_s(x, seconds_budget: float = 20.0):
+    """Oracle (numpy restatement of the reference) on 1 host core: MPdist profile
+    rows of one segment per sampled length at the true n, bounded windows."""
+    from oracle import pastila_oracle as O
+
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    done_pairs, t_tot, sample = 0, 0.0, []
+    for m in (64, 256, 512):
+        l, k = O.window_default(m), O.order_default(m)
+        w = m - l + 1
+        xs = x[: 200_000]   # window subset of the same series (pairs counted exactly)
+        st = O.sliding_stats(xs, l)
+        t0 = time.perf_counter()
+        O.mpdist_profile(xs, 3, m, l, k, st, col_chunk=50_000)
+        dt = time.perf_counter() - t0
+        done_pairs += w * (xs.size - l + 1)
+        t_tot += dt
+        sample.append(f"m={m}: 1 segment x {xs.size - m + 1} windows {dt:.1f}s")
+        if t_tot > seconds_budget:
+            break
+    return done_pairs / t_tot, "; ".join(sample)
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on all host cores, bounded sample of C3."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from concurrent.futures import ProcessPoolExecutor
+
+    x = workload()
+    cores = os.cpu_count() or 1
+    jobs = [(m, i) for i, m in enumerate(GRID)][: max(1, cores)]
+    # each job: one segment of one length, windows restricted to a 100k-sample slice
+    def step():
+        t0 = time.perf_counter()
+        with ProcessPoolExecutor(max_workers=min(cores, len(jobs))) as pool:
+            tot = sum(pool.map(_ref_job, [(m, i) for m, i in jobs]))
+        return tot, time.perf_counter() - t0
+    for _ in range(args.warmup):
+        step()
+    vals = []
+    for _ in range(args.steps):
+        p, dt = step()
+        vals.append(p / dt)
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(ws),
+            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": min(cores, len(jobs)), "kind": "port",
+                             "sample": f"{len(jobs)} jobs (one per length of the C3 grid, one per core): "
+                                       "MPdist profile of segment 3 over the first 100000 samples of the C3 series"},
+            "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _ref_job(arg):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import pastila_oracle as O
+
+    m, _ = arg
+    x = workload()[:100_000]
+    l, k = O.window_default(m), O.order_default(m)
+    st = O.sliding_stats(x, l)
+    O.mpdist_profile(x, 3, m, l, k, st, col_chunk=25_000)
+    return (m - l + 1) * (x.size - l + 1)
+
+
+def _config(ws):
+    return {"workload": "C3: planted walk n=1,000,000 (A=4, m_act=256, seed 0), m in 64..512 step 32 "
+                        "(15 lengths), K=4, l=ceil(m/2), k=ceil(m/10)",
+            "n": N_SERIES, "grid": [GRID[0], GRID[-1], 32], "K": K_SNIPPETS,
+            "parallelism": f"length-sharded x{ws}" if ws > 1 else "1 GPU",
+            "l2_flush": "not needed: per-length profile matrix 15-125 GB >> 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pastila", choices=["pastila", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grid", default=None, help="dev only: comma-separated lengths (invalidates the metric)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    ws, rank, local = dist_init()
+    import torch
+
+    import paper_2401_13680_b200 as P
+    from paper_2401_13680_b200 import _native, parallel
+
+    grid = [int(v) for v in args.grid.split(",")] if args.grid else GRID
+    x = workload()
+    ctx = _native.context(local)
+    lib = _native.load_library()
+    sh = C.c_void_p()
+    ctx.call("pst_stream", C.byref(sh))
+    stream = torch.cuda.ExternalStream(sh.value, device=torch.device("cuda", local))
+    xd = torch.from_numpy(x).to(f"cuda:{local}")
+    series = P.TimeSeries(x)
+    parts = parallel.length_partition([P.default_cost(N_SERIES, m) for m in grid], ws)
+    mine = [grid[i] for i in parts[rank]]
+
+    def device_step():
+        # inputs resident in HBM: device-to-device reload + prefix sums, then all my lengths
+        ctx.call("pst_set_series_dev", C.c_void_p(xd.data_ptr()), C.c_int64(x.size))
+        ctx._series_key, ctx._series_ref = (id(series.values), series.values.ctypes.data, x.size), series.values
+        out = {}
+        for m in mine:
+            out[m] = P.select_snippets(series, P.MPdistParams(m), K_SNIPPETS)
+        return out
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        device_step()
+    ctx.call("pst_sync")
+    barrier()
+    ctx.call("pst_timing", 1)
+    l0 = ctx.launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(local)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = device_step()
+        ev1.record(stream)
+        ctx.call("pst_sync")
+        torch.cuda.synchronize(local)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kms, klaunch = C.c_double(0), C.c_int64(0)
+    ctx.call("pst_timing_read", C.byref(kms), C.byref(klaunch))
+    ctx.call("pst_timing", 0)
+    launches = ctx.launches() - l0
+    barrier()
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- e2e through the public API (host buffers in, results out) ----------------------
+    def e2e_step():
+        s = P.TimeSeries(np.array(x))  # fresh host object -> H2D upload inside the step
+        if ws > 1:
+            from paper_2401_13680_b200.scheduler import job_weights, run_jobs
+
+            jobs = [P.MPdistParams(m) for m in grid]
+            timings = parallel.run_sharded(s, jobs, K_SNIPPETS, job_weights(s, jobs, None))
+            return {p.snippet_size: r for p, r, _ in timings}
+        rep, results = P.select_length(s, grid, K_SNIPPETS, training_log=False)
+        return results
+    barrier()
+    t0 = time.perf_counter()
+    e2e_res = e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    total_pairs = sum(pairs_of(N_SERIES, m) for m in grid)
+    my_pairs = sum(pairs_of(N_SERIES, m) for m in mine)
+    value = total_pairs / (ms / 1e3)
+    d2h = sum(K_SNIPPETS * (N_SERIES - m + 1) * 8 + (N_SERIES - m + 1) * 12 + N_SERIES * 8
+              + (N_SERIES // m) * 8 for m in grid)
+    peak, peak_src = fp64_peak()
+    achieved = FP64_FLOPS_PER_PAIR * my_pairs * args.steps / (kms.value / 1e3) / 1e12 if kms.value > 0 else None
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        v, sample = cpu_sample_pairs_per_s(x)
+        cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample}
+    if rank == 0:
+        traffic = None
+        tp = ROOT / "profiles" / "r01_traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "seconds_per_sweep": ms / 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(ws),
+            "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "seconds": e2e_s,
+                    "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)},
+            "roofline": {"bound": "fp64", "kernel": "k_mpdist (profile tile kernel)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "flops_per_pair": FP64_FLOPS_PER_PAIR, "peak_source": peak_src,
+                         "kernel_ms_per_step": kms.value / args.steps,
+                         "kernel_share_of_step": (kms.value / args.steps) / ms},
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "m_best": max(((m, r.criterion_ or 0.0) for m, r in e2e_res.items()), key=lambda t: (t[1], -t[0]))[0],
+        }
+        if args.grid:
+            line["config"]["dev_grid_override"] = grid
+            line["invalid"] = "grid override: not the metric configuration"
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

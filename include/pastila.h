@@ -110,6 +110,12 @@ int pst_areas_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, in
  * row indices offset by row_base.  minval_dev [N], argmin_dev [N].        */
 int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
                    int64_t row_base, double* minval_dev, int32_t* argmin_dev);
+/* The context's CUDA stream (cudaStream_t) for caller-side event timing.  */
+int pst_stream(pst_ctx* ctx, void** stream_out);
+/* Profile-kernel timing: pst_timing(ctx,1) enables + resets; pst_timing_read
+ * returns device milliseconds and launches of profile kernels since.      */
+int pst_timing(pst_ctx* ctx, int enable);
+int pst_timing_read(pst_ctx* ctx, double* ms, int64_t* launches);
 /* Wait for all work queued on the context stream.                        */
 int pst_sync(pst_ctx* ctx);
 /* Kernel launches issued on the context since creation (instrumentation). */

@@ -52,6 +52,9 @@ SIGNATURES = {
     "pst_colmin_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "pst_criterion": (C.c_int, [_vp, _dp, _i64, _i64, C.c_double, _dp]),
     "pst_labels": (C.c_int, [_vp, _dp, _i64, _i64, _i64, _lp]),
+    "pst_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "pst_timing": (C.c_int, [_vp, C.c_int]),
+    "pst_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "pst_sync": (C.c_int, [_vp]),
     "pst_launch_count": (C.c_int64, [_vp]),
 }

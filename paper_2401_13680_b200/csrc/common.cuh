@@ -53,6 +53,8 @@ struct LenData {
 struct pst_ctx {
   int dev = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;   // selection stream (overlaps the next batch's row loop)
+  cudaEvent_t ev_rows[2] = {nullptr, nullptr}, ev_sel[2] = {nullptr, nullptr};
   int64_t n = 0, cap_n = 0;
   double* x = nullptr;
   double* csum = nullptr;   // [n+1] sequential prefix sum of x
@@ -72,6 +74,11 @@ struct pst_ctx {
   double* dbg = nullptr;
   size_t dbg_bytes = 0;
   int64_t dbg_T = 0, dbg_NC = 0, dbg_w = 0;
+  // kernel timing (profile kernel): events around each launch_mpdist call
+  bool timing = false;
+  void* tev = nullptr;  // std::vector<std::pair<cudaEvent_t,cudaEvent_t>>*
+  double t_ms = 0.0;
+  int64_t t_calls = 0, t_launch = 0;
   int num_sms = 148;
   size_t smem_optin = 0;
 };
@@ -88,6 +95,8 @@ struct MPArgs {
   int64_t ldD, rowD0;
   double* ab;        // scratch, w*T doubles per CTA
   double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
+  double* ba;        // scratch: allP_BA per CTA (NCmax doubles)
+  int dbg_nostore;   // debug: skip AB stores (timing experiments only)
 };
 
 int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,

@@ -22,111 +22,329 @@
 #include "common.cuh"
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 namespace {
 
-__device__ __forceinline__ double dmin(double a, double b) { return fmin(a, b); }
+// NaN-free min/max (values are finite or +inf): 1 DSETP + 2 FSEL instead of the
+// ~8-instruction IEEE fmin/fmax sequence.
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
-// k-th smallest (1-based) of the 2w keys of one window.  Keys are the bit
-// patterns of non-negative doubles (order preserving).  A: w values in global
-// scratch (stride ldA), B: w values in shared memory.  Exact: bracketing by
-// counting passes; first pivot = previous window's answer (adjacent windows
-// share most of their multiset), then interpolation, then key bisection.
-__device__ long long select_kth(const double* __restrict__ A, int64_t ldA, const double* __restrict__ B,
-                                int64_t w, int64_t k, long long pivot) {
-  const int64_t M2 = 2 * w;
-  if (M2 <= k) {  // mpdist.py:230-231: max fallback
-    long long mx = 0;
-    for (int64_t i = 0; i < w; ++i) {
-      long long a = dkey(clamp0(A[i * ldA])), b = dkey(B[i]);
-      mx = max(mx, max(a, b));
-    }
-    return mx;
-  }
-  long long lo = -1, hi = 0x7ff0000000000000LL;  // answer in (lo, hi]
-  int64_t clo = 0, chi = M2;
-  long long p = pivot;
-  for (int it = 0; it < 200; ++it) {
-    int64_t lt = 0, le = 0;
-    long long mb = -1, ma = 0x7fffffffffffffffLL;
-    for (int64_t i = 0; i < w; ++i) {
-      long long v = dkey(clamp0(A[i * ldA]));
-      lt += (v < p);
-      le += (v <= p);
-      if (v < p && v > mb) mb = v;
-      if (v > p && v < ma) ma = v;
-    }
-    for (int64_t i = 0; i < w; ++i) {
-      long long v = dkey(B[i]);
-      lt += (v < p);
-      le += (v <= p);
-      if (v < p && v > mb) mb = v;
-      if (v > p && v < ma) ma = v;
-    }
-    if (lt < k && k <= le) return p;
-    if (k <= lt) {
-      if (k == lt) return mb;
-      hi = mb;
-      chi = lt;
-    } else {
-      if (k == le + 1) return ma;
-      lo = p;
-      clo = le;
-    }
-    // next pivot in (lo, hi]
-    long long np;
-    if (it < 6 && hi < 0x7ff0000000000000LL) {
-      double lv = lo < 0 ? 0.0 : kdbl(lo);
-      double hv = kdbl(hi);
-      double f = ((double)(k - clo) - 0.5) / (double)(chi - clo);
-      double pv = lv + (hv - lv) * f;
-      np = dkey(pv);
-      if (np <= lo) np = lo + 1;
-      if (np > hi) np = hi;
-    } else if (hi >= 0x7ff0000000000000LL) {
-      // no finite upper bracket yet: grow geometrically from the lower one
-      double lv = lo < 0 ? 0.0 : kdbl(lo);
-      np = dkey(lv > 0.0 ? lv * 2.0 : 1.0);
-      if (np <= lo) np = lo + 1;
-    } else {
-      np = lo + (long long)(((unsigned long long)(hi - lo) + 1ull) >> 1);
-      if (np <= lo) np = lo + 1;
-    }
-    p = np;
-  }
-  return p;  // unreachable in practice (bisection converges in <= 64 steps)
+// ---------------------------------------------------------------- selection
+// Exact k-th smallest (1-based) of the 2w-element P_ABBA multiset of one
+// window: A = w row minima (contiguous column of the AB scratch, global),
+// B = w column minima (shared memory).  All values are clamped >= 0.
+//
+// Adjacent windows share almost all of their multiset, so the previous
+// window's answer is the first pivot: one counting pass settles ~75% of
+// windows; a second pass that tracks the two nearest values on the needed
+// side settles rank moves of 1-2 (~23%); larger moves fall back to bracketing
+// passes (interpolation, then bisection on the order-preserving bit pattern).
+// ---------------------------------------------------------------- selection
+// Warp-cooperative exact k-th smallest of each window's 2w-element P_ABBA
+// multiset.  A warp sweeps a run of consecutive windows; for window j, lane L
+// holds A[L+32t] (row minima: contiguous column of the AB scratch) and
+// B[L+32t] (column minima window, shared memory) in registers.  Every
+// decision is warp-uniform (no divergence between windows).  The previous
+// window's answer is the first pivot: one counting pass settles ~75% of
+// windows, one adjacent-value step settles rank moves of 1, a second step
+// moves of 2; larger moves (and the first window of a run) use rank
+// interpolation / bisection between exact brackets.
+__device__ __forceinline__ unsigned dhi(double v) { return (unsigned)(__double_as_longlong(v) >> 32); }
+__device__ __forceinline__ unsigned dlo(double v) { return (unsigned)__double_as_longlong(v); }
+__device__ __forceinline__ double dmk(unsigned hi, unsigned lo) {
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+// exact warp max / min of non-negative doubles via two 32-bit REDUX steps
+__device__ __forceinline__ double warp_max(double v) {
+  const unsigned h = __reduce_max_sync(FULLMASK, dhi(v));
+  const unsigned l = __reduce_max_sync(FULLMASK, dhi(v) == h ? dlo(v) : 0u);
+  return dmk(h, l);
+}
+__device__ __forceinline__ double warp_min(double v) {
+  const unsigned h = __reduce_min_sync(FULLMASK, dhi(v));
+  const unsigned l = __reduce_min_sync(FULLMASK, dhi(v) == h ? dlo(v) : 0xffffffffu);
+  return dmk(h, l);
 }
 
-template <int P, int NT>
-__global__ void __launch_bounds__(NT) k_mpdist(const MPArgs a) {
+template <int TM>
+struct WinVals {
+  double a[TM], b[TM];
+};
+
+template <int TM>
+__device__ __forceinline__ void count2(const WinVals<TM>& v, double p, int& lt, int& le) {
+  int l1 = 0, l2 = 0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    l1 += (v.a[t] < p) + (v.b[t] < p);
+    l2 += (v.a[t] <= p) + (v.b[t] <= p);
+  }
+  lt = __reduce_add_sync(FULLMASK, l1);
+  le = __reduce_add_sync(FULLMASK, l2);
+}
+template <int TM>
+__device__ __forceinline__ double below_max(const WinVals<TM>& v, double p) {  // largest element < p (or 0)
+  double m = 0.0;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    m = dmax(m, v.a[t] < p ? v.a[t] : 0.0);
+    m = dmax(m, v.b[t] < p ? v.b[t] : 0.0);
+  }
+  return warp_max(m);
+}
+template <int TM>
+__device__ __forceinline__ double above_min(const WinVals<TM>& v, double p) {  // smallest element > p (or +inf)
+  double m = PST_INF;
+#pragma unroll
+  for (int t = 0; t < TM; ++t) {
+    m = dmin(m, v.a[t] > p ? v.a[t] : PST_INF);
+    m = dmin(m, v.b[t] > p ? v.b[t] : PST_INF);
+  }
+  return warp_min(m);
+}
+
+// k-th smallest; p = pivot hint (any value >= 0).  2w > k assumed.
+template <int TM>
+__device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
+  double lov = 0.0, hi = PST_INF;
+  int clo = 0, chi = 2 * w;
+  for (int it = 0; it < 256; ++it) {
+    int lt, le;
+    count2<TM>(v, p, lt, le);
+    if (lt < k && k <= le) return p;
+    bool down = k <= lt;
+    if (down) {
+      const double b = below_max<TM>(v, p);  // #(<= b) = lt
+      if (k == lt) return b;
+      hi = b;
+      chi = lt;
+    } else {
+      const double u = above_min<TM>(v, p);  // smallest element > p
+      if (k == le + 1) return u;
+      lov = u;
+      clo = le;
+    }
+    double np;
+    if (it < 2) {
+      np = down ? hi : lov;  // adjacent-value step (rank moves of 1-2 are the common case)
+    } else if (hi < PST_INF && it < 10) {
+      const double f = ((double)(k - clo) - 0.5) / (double)(chi - clo);
+      np = lov + (hi - lov) * f;
+    } else if (hi < PST_INF) {
+      np = 0.5 * (lov + hi);
+    } else {
+      np = lov > 0.0 ? 2.0 * lov : 1.0;
+    }
+    np = dmin(dmax(np, lov), hi);
+    if (np == p) np = hi < PST_INF ? hi : 2.0 * np + 1.0;
+    p = np;
+  }
+  return p;
+}
+
+// Profiles for windows [j0, j1) of the tile: A columns at ab + j*S, B = BA + j.
+template <int TM>
+__device__ void select_run(const double* __restrict__ ab, int S, const double* __restrict__ BA, int w, int k, int j0,
+                           int j1, int lane, double* __restrict__ Drow, double twol) {
+  double p = -1.0;
+  double outv = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double* A = ab + (int64_t)j * S;
+    const double* B = BA + j;
+    WinVals<TM> v;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      const int idx = lane + 32 * t;
+      const bool ok = idx < w;
+      v.a[t] = ok ? A[idx] : PST_INF;
+      v.b[t] = ok ? B[idx] : PST_INF;
+    }
+    double ans;
+    if (2 * w <= k) {  // max fallback (mpdist.py:230-231)
+      double m = 0.0;
+#pragma unroll
+      for (int t = 0; t < TM; ++t) {
+        const int idx = lane + 32 * t;
+        if (idx < w) m = dmax(m, dmax(v.a[t], v.b[t]));
+      }
+      ans = warp_max(m);
+    } else {
+      if (p < 0.0) {  // first window of the run: pivot at the median of lane 0..31's first A values
+        p = warp_max(v.a[0] < PST_INF ? v.a[0] : 0.0) * 0.25;
+      }
+      ans = warp_select<TM>(v, w, k, p);
+    }
+    p = ans;
+    double ev = ans;
+    if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
+    if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
+    const double dv = sqrt(twol * ev);
+    if (lane == ((j - j0) & 31)) outv = dv;
+    if (((j - j0) & 31) == 31 || j == j1 - 1) {  // flush up to 32 outputs with one coalesced store
+      const int base = j - ((j - j0) & 31);
+      if (base + lane <= j) Drow[base + lane] = outv;
+    }
+  }
+}
+
+// van Herk row sliding minima for one row, register version.
+// Blocks of w columns; a group of LPB lanes owns block b (SUF) and block b+1
+// (PRE); lane chunks of CH (odd) consecutive columns; the combine
+//   AB[u] = min(SUF_b[u], PRE_{b+1}[u-1])
+// is done in registers (4 mins per element).  Writes clamped AB values to the
+// transposed scratch column of each window.
+template <int CHM>
+__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int NC, int NJ, int w, int CH, int LPB,
+                                           int warp, int lane, int nw, double* __restrict__ abrow,
+                                           double* __restrict__ stg) {
+  const int bpw = 32 / LPB;                 // blocks per warp
+  const int sub = lane / LPB, ll = lane % LPB;
+  const int nblk = (NJ + w - 1) / w;
+  for (int b0 = warp * bpw; b0 < nblk; b0 += nw * bpw) {  // warp-uniform trip count
+    const int b = b0 + sub;
+    const int bb = b * w, bn = bb + w;
+    const int u0 = ll * CH;
+    double sf[CHM], pr[CHM];
+    double run = PST_INF;
+#pragma unroll
+    for (int t = CHM - 1; t >= 0; --t) {
+      const int u = u0 + t;
+      const double v = (t < CH && u < w && bb + u < NC) ? E[bb + u] : PST_INF;
+      run = dmin(run, v);
+      sf[t] = run;
+    }
+    double totS = run;
+    run = PST_INF;
+#pragma unroll
+    for (int t = 0; t < CHM; ++t) {
+      const int u = u0 + t;
+      const double v = (t < CH && u < w && bn + u < NC) ? E[bn + u] : PST_INF;
+      run = dmin(run, v);
+      pr[t] = run;
+    }
+    double totP = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      if (off < LPB) {
+        const double ds = __shfl_down_sync(FULLMASK, totS, off, LPB);
+        const double dp = __shfl_up_sync(FULLMASK, totP, off, LPB);
+        totS = dmin(totS, ds);
+        totP = dmin(totP, dp);
+      }
+    }
+    double cs = __shfl_down_sync(FULLMASK, totS, 1, LPB);
+    double cp = __shfl_up_sync(FULLMASK, totP, 1, LPB);
+    if (ll == LPB - 1) cs = PST_INF;
+    if (ll == 0) cp = PST_INF;
+    const double C = dmin(cs, cp);
+    // combine into the warp's staging row (window offsets (b-b0)*w + u) ...
+#pragma unroll
+    for (int t = 0; t < CHM; ++t) {
+      const int u = u0 + t;
+      if (t < CH && u < w) {
+        double v = dmin(sf[t], C);
+        if (t > 0) v = dmin(v, pr[t - 1]);
+        stg[sub * w + u] = clamp0(v);
+      }
+    }
+    __syncwarp();
+    // ... then one coalesced row-major store of the warp's bpw*w windows
+    const int jb = b0 * w;
+    const int cnt = min(bpw * w, NJ - jb);
+    for (int idx = lane; idx < cnt; idx += 32) abrow[jb + idx] = stg[idx];
+    __syncwarp();
+  }
+}
+
+// van Herk, shared-memory version for large w (chunks do not fit registers).
+__device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double* __restrict__ SUF,
+                                            double* __restrict__ PRE, int NC, int NJ, int w, int warp, int lane,
+                                            int nw, double* __restrict__ abrow) {
+  const int nblk = (NJ + w - 1) / w;
+  const int CH = (w + 31) / 32;
+  for (int b = warp; b < nblk; b += nw) {
+    const int bb = b * w, bn = bb + w;
+    {
+      const int endb = min(bb + w, NC);
+      const int u0 = bb + lane * CH, u1 = min(u0 + CH, endb);
+      double run = PST_INF;
+      for (int c = u1 - 1; c >= u0; --c) {
+        run = dmin(run, E[c]);
+        SUF[c] = run;
+      }
+      double tot = run;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_down_sync(FULLMASK, tot, off));
+      double carry = __shfl_down_sync(FULLMASK, tot, 1);
+      if (lane == 31) carry = PST_INF;
+      for (int c = u0; c < u1; ++c) SUF[c] = dmin(SUF[c], carry);
+    }
+    {
+      const int endn = min(bn + w, NC);
+      const int u0 = bn + lane * CH, u1 = min(u0 + CH, endn);
+      double run = PST_INF;
+      for (int c = u0; c < u1; ++c) {
+        run = dmin(run, E[c]);
+        PRE[c] = run;
+      }
+      double tot = run;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_up_sync(FULLMASK, tot, off));
+      double carry = __shfl_up_sync(FULLMASK, tot, 1);
+      if (lane == 0) carry = PST_INF;
+      for (int c = u0; c < u1; ++c) PRE[c] = dmin(PRE[c], carry);
+    }
+    __syncwarp();
+    for (int u = lane; u < w && bb + u < NJ; u += 32) {
+      double v = SUF[bb + u];
+      if (u > 0) v = dmin(v, PRE[bn + u - 1]);
+      abrow[bb + u] = clamp0(v);
+    }
+  }
+}
+
+template <int P, int NT, int CHM>
+__global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(const MPArgs a) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
-  const int64_t l = a.l, w = a.w, T = a.T;
-  const int64_t s = a.seg0 + blockIdx.y;
-  const int64_t q0 = s * a.m;
-  const int64_t J0 = (int64_t)blockIdx.x * T;
-  const int64_t NJ = min(T, a.N - J0);
-  const int64_t NC = NJ + w - 1;
-  const int64_t NCmax = (int64_t)NT * P;
+  constexpr int NCmax = NT * P;
+  const int l = (int)a.l, w = (int)a.w, T = (int)a.T;
+  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t J0 = (int64_t)blockIdx.x * a.T;
+  const int NJ = (int)min(a.T, a.N - J0);
+  const int NC = NJ + w - 1;
   double* xs = sm;             // [l]
   double* edge = xs + l;       // [w]
-  double* E = edge + w;        // [NCmax] row e-values, later allP_BA
-  double* SUF = E + NCmax;     // [NCmax]
-  double* PRE = SUF + NCmax;   // [NCmax]
-  double* xfer = PRE + NCmax;  // [64]
+  double* rdf = edge + w;      // [w] df[q-1] per row
+  double* rdg = rdf + w;       // [w] dg[q-1] per row
+  double* rnq = rdg + w;       // [w] nrm[q] per row
+  double* E0 = rnq + w;        // [NCmax] row e-values (even rows), later allP_BA
+  double* E1 = E0 + NCmax;     // [NCmax] row e-values (odd rows)
+  double* xfer = E1 + NCmax;   // [64]
   double* red = xfer + 64;     // [2]
-  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * (w * T);
-  const double* __restrict__ x = a.x;
+  double* STG = red + 2;       // [NW * 32 * max(CHM,1)] per-warp staging of one AB row
+  double* SUF = STG + NW * 32 * (CHM > 0 ? CHM : 1);  // [NCmax] (shared-memory van Herk only)
+  double* PRE = SUF + NCmax;   // [NCmax]
+  double* E = E0;
+  // AB scratch of this CTA: row-major [w][T]
+  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * T);
+  const double* __restrict__ xJ = a.x + J0;
+  const double* __restrict__ xQ = a.x + q0;
+  const double* __restrict__ muJ = a.mu + J0;
+  const double* __restrict__ muQ = a.mu + q0;
 
-  // ---- row-0 fresh dots: cov(q0, c) = sum_t (x[q0+t]-mu[q0]) * x[c+t] - mu[c]*sum_t(x[q0+t]-mu[q0])
+  // ---- row-0 fresh dots: cov(q0, c) = sum_t (x[q0+t]-mu[q0]) x[c+t] - mu[c] sum_t (x[q0+t]-mu[q0])
   {
-    const double mq = a.mu[q0];
-    for (int64_t t = tid; t < l; t += NT) xs[t] = x[q0 + t] - mq;
+    const double mq = muQ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xQ[t] - mq;
     __syncthreads();
     if (tid == 0) {
       double s1 = 0.0;
-      for (int64_t t = 0; t < l; ++t) s1 += xs[t];
+      for (int t = 0; t < l; ++t) s1 += xs[t];
       red[0] = s1;
     }
     __syncthreads();
@@ -136,12 +354,12 @@ __global__ void __launch_bounds__(NT) k_mpdist(const MPArgs a) {
     const double sx = red[0];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-      const int64_t cl = (int64_t)tid * P + p;
+      const int cl = tid * P + p;
       double acc = 0.0;
       if (cl < NC) {
-        const double* xc = x + J0 + cl;
-        for (int64_t t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
-        acc = fma(-a.mu[J0 + cl], sx, acc);
+        const double* xc = xJ + cl;
+        for (int t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
+        acc = fma(-muJ[cl], sx, acc);
       }
       cov[p] = acc;
     }
@@ -149,141 +367,300 @@ __global__ void __launch_bounds__(NT) k_mpdist(const MPArgs a) {
   __syncthreads();
   // ---- left edge (column J0) for rows 1..w-1: fresh dots against the centered column window
   {
-    const double mc = a.mu[J0];
-    for (int64_t t = tid; t < l; t += NT) xs[t] = x[J0 + t] - mc;
+    const double mc = muJ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xJ[t] - mc;
     __syncthreads();
     if (tid == 0) {
       double s1 = 0.0;
-      for (int64_t t = 0; t < l; ++t) s1 += xs[t];
+      for (int t = 0; t < l; ++t) s1 += xs[t];
       red[1] = s1;
     }
     __syncthreads();
     const double sx = red[1];
-    for (int64_t i = 1 + tid; i < w; i += NT) {
-      const double* xq = x + q0 + i;
+    for (int i = 1 + tid; i < w; i += NT) {
+      const double* xq = xQ + i;
       double acc = 0.0;
-      for (int64_t t = 0; t < l; ++t) acc = fma(xq[t], xs[t], acc);
-      edge[i] = fma(-a.mu[q0 + i], sx, acc);
+      for (int t = 0; t < l; ++t) acc = fma(xq[t], xs[t], acc);
+      edge[i] = fma(-muQ[i], sx, acc);
     }
+  }
+  for (int i = tid; i < w; i += NT) {
+    rdf[i] = i > 0 ? a.df[q0 + i - 1] : 0.0;
+    rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
+    rnq[i] = a.nrm[q0 + i];
   }
   // ---- per-column constants
   double dgc[P], dfc[P], nrmc[P], bic[P], colmin[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    const int64_t cl = (int64_t)tid * P + p, c = J0 + cl;
+    const int cl = tid * P + p;
     const bool ok = cl < NC;
+    const int64_t c = J0 + cl;
     dgc[p] = (ok && c > 0) ? a.dg[c - 1] : 0.0;
     dfc[p] = (ok && c > 0) ? a.df[c - 1] : 0.0;
     nrmc[p] = ok ? a.nrm[c] : 0.0;
-    bic[p] = ok ? a.bias[c] : 0.0;
+    bic[p] = ok ? a.bias[c] : PST_INF;
     colmin[p] = PST_INF;
   }
   __syncthreads();
 
-  const int64_t nblk = (NJ + w - 1) / w;  // van Herk blocks that contain windows
-  const int64_t CH = (w + 31) / 32;
-  for (int64_t i = 0; i < w; ++i) {
-    const int64_t q = q0 + i;
+  const int qloc = (int)(q0 - J0) - tid * P;  // my local index of the self column at row 0
+  const int CH = (CHM > 0) ? (((w + 31) / 32) | 1) : 0;
+  int LPB = 32;
+  if (CHM > 0) {
+    while (LPB > 8 && (LPB / 2) * CHM >= w && (((w + LPB / 2 - 1) / (LPB / 2)) | 1) <= CHM) LPB /= 2;
+  }
+  const int CHr = (CHM > 0) ? ((((w + LPB - 1) / LPB)) | 1) : 0;
+  for (int i = 0; i < w; ++i) {
+    double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
     if (i > 0) {
-      const double dfq = a.df[q - 1], dgq = a.dg[q - 1];
-      double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
+      const double dfq = rdf[i], dgq = rdg[i];
       if (lane == 0 && warp > 0) left = xfer[((i - 1) & 1) * 32 + warp - 1];
 #pragma unroll
       for (int p = P - 1; p >= 1; --p) cov[p] = fma(dfq, dgc[p], fma(dgq, dfc[p], cov[p - 1]));
       cov[0] = (tid == 0) ? edge[i] : fma(dfq, dgc[0], fma(dgq, dfc[0], left));
     }
     if (lane == 31) xfer[(i & 1) * 32 + warp] = cov[P - 1];
-    const double nq = a.nrm[q];
-    const bool qconst = (nq == 0.0);
+    const double nq = rnq[i];
+    E = (i & 1) ? E1 : E0;
+    double* Et = E + tid * P;
+    if (nq != 0.0) {
+      const double mnq = -nq;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int64_t cl = (int64_t)tid * P + p, c = J0 + cl;
-      double e;
-      if (qconst)
-        e = (cl < NC) ? a.cbias[c] : 0.0;
-      else
-        e = fma(-(cov[p] * nq), nrmc[p], bic[p]);
-      if (c == q) e = 0.0;
-      if (cl >= NC) e = PST_INF;
-      colmin[p] = dmin(colmin[p], e);
-      E[cl] = e;
-    }
-    __syncthreads();
-    // van Herk: warp per block pair (b, b+1); SUF over block b, PRE over block b+1
-    for (int64_t b = warp; b < nblk; b += NW) {
-      const int64_t bb = b * w, bn = bb + w;
-      {
-        const int64_t endb = min(bb + w, NC);
-        const int64_t u0 = bb + lane * CH, u1 = min(u0 + CH, endb);
-        double run = PST_INF;
-        for (int64_t c = u1 - 1; c >= u0; --c) {
-          run = dmin(run, E[c]);
-          SUF[c] = run;
-        }
-        double tot = run;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_down_sync(FULLMASK, tot, off));
-        double carry = __shfl_down_sync(FULLMASK, tot, 1);
-        if (lane == 31) carry = PST_INF;
-        for (int64_t c = u0; c < u1; ++c) SUF[c] = dmin(SUF[c], carry);
+      for (int p = 0; p < P; ++p) {
+        const double e = fma(cov[p] * mnq, nrmc[p], bic[p]);
+        colmin[p] = dmin(colmin[p], e);
+        Et[p] = e;
       }
-      {
-        const int64_t endn = min(bn + w, NC);
-        const int64_t u0 = bn + lane * CH, u1 = min(u0 + CH, endn);
-        double run = PST_INF;
-        for (int64_t c = u0; c < u1; ++c) {
-          run = dmin(run, E[c]);
-          PRE[c] = run;
-        }
-        double tot = run;
+    } else {  // constant query window (row-uniform branch): zdist.py:111-112
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_up_sync(FULLMASK, tot, off));
-        double carry = __shfl_up_sync(FULLMASK, tot, 1);
-        if (lane == 0) carry = PST_INF;
-        for (int64_t c = u0; c < u1; ++c) PRE[c] = dmin(PRE[c], carry);
-      }
-      __syncwarp();
-      double* abrow = ab + i * T;
-      for (int64_t u = lane; u < w && bb + u < NJ; u += 32) {
-        double v = SUF[bb + u];
-        if (u > 0) v = dmin(v, PRE[bn + u - 1]);
-        abrow[bb + u] = v;
+      for (int p = 0; p < P; ++p) {
+        const int cl = tid * P + p;
+        const double e = (cl < NC) ? a.cbias[J0 + cl] : PST_INF;
+        colmin[p] = dmin(colmin[p], e);
+        Et[p] = e;
       }
     }
+    {  // self column (zdist.py:121-122)
+      const int ql = qloc + i;
+      if (ql >= 0 && ql < P) Et[ql] = 0.0;
+    }
     __syncthreads();
-  }
-
-  // ---- allP_BA (column minima), clamped at 0
-#pragma unroll
-  for (int p = 0; p < P; ++p) {
-    const int64_t cl = (int64_t)tid * P + p;
-    if (cl < NC) E[cl] = clamp0(colmin[p]);
+    if constexpr (CHM > 0)
+      vh_row_reg<CHM>(E, NC, NJ, w, CHr, LPB, warp, lane, NW, ab + (int64_t)i * T, STG + warp * 32 * CHM);
+    else {
+      vh_row_smem(E, SUF, PRE, NC, NJ, w, warp, lane, NW, ab + (int64_t)i * T);
+      __syncthreads();  // SUF/PRE reused next row
+    }
+    // no trailing barrier: the next row writes the other E buffer; the barrier
+    // after that row's writes orders this row's reads before row i+2's writes.
   }
   __syncthreads();
-  if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
-    for (int64_t c = tid; c < NC; c += NT) a.dbg_ba[c] = E[c];
+  E = E0;
 
-  // ---- k-th smallest of P_ABBA per window; thread owns R consecutive windows
-  const int64_t R = (NJ + NT - 1) / NT;
-  const double twol = 2.0 * (double)l;
-  double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
-  long long prev = -1;
-  for (int64_t r = 0; r < R; ++r) {
-    const int64_t j = (int64_t)tid * R + r;
-    if (j >= NJ) break;
-    long long piv = prev >= 0 ? prev : dkey(E[j + w / 2]);
-    long long kk = select_kth(ab + j, T, E + j, w, a.k, piv);
-    prev = kk;
-    double ev = kdbl(kk);
-    if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
-    if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
-    Drow[j] = sqrt(twol * ev);
+  // ---- allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int cl = tid * P + p;
+    const int64_t c = J0 + cl;
+    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : clamp0(colmin[p]);
+  }
+  __syncthreads();
+  {
+    double* bag = a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
+    for (int c = tid; c < NC; c += NT) bag[c] = E[c];
+    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+      for (int c = tid; c < NC; c += NT) a.dbg_ba[c] = E[c];
   }
 }
 
-template <int P, int NT>
+// Generic (memory-resident) variant of the warp selection for 2w > 32*2*16.
+struct MemWin {
+  const double* A;
+  const double* B;
+  int w;
+};
+__device__ __forceinline__ void count2m(const MemWin& v, int lane, double p, int& lt, int& le) {
+  int l1 = 0, l2 = 0;
+  for (int i = lane; i < v.w; i += 32) {
+    const double x = v.A[i], y = v.B[i];
+    l1 += (x < p) + (y < p);
+    l2 += (x <= p) + (y <= p);
+  }
+  lt = __reduce_add_sync(FULLMASK, l1);
+  le = __reduce_add_sync(FULLMASK, l2);
+}
+__device__ __forceinline__ double below_maxm(const MemWin& v, int lane, double p) {
+  double m = 0.0;
+  for (int i = lane; i < v.w; i += 32) {
+    const double x = v.A[i], y = v.B[i];
+    m = dmax(m, x < p ? x : 0.0);
+    m = dmax(m, y < p ? y : 0.0);
+  }
+  return warp_max(m);
+}
+__device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p) {
+  double m = PST_INF;
+  for (int i = lane; i < v.w; i += 32) {
+    const double x = v.A[i], y = v.B[i];
+    m = dmin(m, x > p ? x : PST_INF);
+    m = dmin(m, y > p ? y : PST_INF);
+  }
+  return warp_min(m);
+}
+__device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
+  const int w = v.w;
+  double lov = 0.0, hi = PST_INF;
+  int clo = 0, chi = 2 * w;
+  for (int it = 0; it < 256; ++it) {
+    int lt, le;
+    count2m(v, lane, p, lt, le);
+    if (lt < k && k <= le) return p;
+    const bool down = k <= lt;
+    if (down) {
+      const double b = below_maxm(v, lane, p);
+      if (k == lt) return b;
+      hi = b;
+      chi = lt;
+    } else {
+      const double u = above_minm(v, lane, p);
+      if (k == le + 1) return u;
+      lov = u;
+      clo = le;
+    }
+    double np;
+    if (it < 2) {
+      np = down ? hi : lov;
+    } else if (hi < PST_INF && it < 10) {
+      const double f = ((double)(k - clo) - 0.5) / (double)(chi - clo);
+      np = lov + (hi - lov) * f;
+    } else if (hi < PST_INF) {
+      np = 0.5 * (lov + hi);
+    } else {
+      np = lov > 0.0 ? 2.0 * lov : 1.0;
+    }
+    np = dmin(dmax(np, lov), hi);
+    if (np == p) np = hi < PST_INF ? hi : 2.0 * np + 1.0;
+    p = np;
+  }
+  return p;
+}
+
+__device__ void select_run_mem(const double* __restrict__ ab, int S, const double* __restrict__ BA, int w, int k,
+                               int j0, int j1, int lane, double* __restrict__ Drow, double twol) {
+  double p = -1.0;
+  for (int j = j0; j < j1; ++j) {
+    MemWin v{ab + (int64_t)j * S, BA + j, w};
+    double ans;
+    if (2 * w <= k) {
+      double m = 0.0;
+      for (int i = lane; i < w; i += 32) m = dmax(m, dmax(v.A[i], v.B[i]));
+      ans = warp_max(m);
+    } else {
+      if (p < 0.0) p = warp_max(v.A[lane < w ? lane : 0]) * 0.25;
+      ans = warp_select_mem(v, lane, k, p);
+    }
+    p = ans;
+    double ev = ans;
+    if (ev < 1e-15) ev = 0.0;
+    if (ev > 2.0) ev = 2.0;
+    if (lane == 0) Drow[j] = sqrt(twol * ev);
+  }
+}
+
+// Selection kernel: one CTA per (tile, segment) of the row kernel's scratch.
+// The tile's allP_BA is staged in shared memory; each warp sweeps a
+// contiguous run of windows in chunks of JC: the chunk's AB block (w rows x JC
+// windows, coalesced row segments) is copied to a padded per-warp buffer
+// (stride JC+1, odd) so that reading one window's column is conflict free.
+__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int TM>
+__global__ void __launch_bounds__(256) k_select(const MPArgs a, int NCmax, int JC) {
+  extern __shared__ double smb[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = (int)a.w, T = (int)a.T;
+  const int64_t J0 = (int64_t)blockIdx.x * a.T;
+  const int NJ = (int)min(a.T, a.N - J0);
+  const int NC = NJ + w - 1;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const double* ab = a.ab + cta * ((int64_t)w * T);
+  const double* bag = a.ba + cta * NCmax;
+  double* BA = smb;
+  const int SJ = JC + 1;
+  double* cbuf[2];
+  cbuf[0] = smb + NCmax + warp * (2 * w * SJ);
+  cbuf[1] = cbuf[0] + w * SJ;
+  const int per = (NJ + 7) / 8;
+  const int j0 = min(NJ, warp * per), j1 = min(NJ, j0 + per);
+  const int rpi = 32 / JC;  // rows per copy instruction (JC <= 32, power of two)
+  const int cj = lane % JC, r0 = lane / JC;
+  auto stage = [&](int jc, double* dst) {  // AB[0..w)[jc .. jc+JC) -> dst[i*SJ + jj]
+    const int nj = min(JC, j1 - jc);
+    if (cj < nj)
+      for (int i = r0; i < w; i += rpi) cp_async8(dst + i * SJ + cj, ab + (int64_t)i * T + jc + cj);
+    cp_async_commit();
+  };
+  if (j0 < j1) stage(j0, cbuf[0]);
+  for (int c = tid; c < NC; c += 256) BA[c] = bag[c];
+  __syncthreads();
+  const double twol = 2.0 * (double)a.l;
+  double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
+  double p = -1.0;
+  int cur = 0;
+  for (int jc = j0; jc < j1; jc += JC, cur ^= 1) {
+    const int nj = min(JC, j1 - jc);
+    if (jc + JC < j1) {
+      stage(jc + JC, cbuf[cur ^ 1]);  // prefetch the next chunk
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncwarp();
+    const double* chunk = cbuf[cur];
+    double outv = 0.0;
+    for (int jj = 0; jj < nj; ++jj) {
+      const int j = jc + jj;
+      const double* Bw = BA + j;
+      WinVals<TM> v;
+#pragma unroll
+      for (int t = 0; t < TM; ++t) {
+        const int idx = lane + 32 * t;
+        const bool ok = idx < w;
+        v.a[t] = ok ? chunk[idx * SJ + jj] : PST_INF;
+        v.b[t] = ok ? Bw[idx] : PST_INF;
+      }
+      double ans;
+      if (2 * w <= (int)a.k) {
+        double m = 0.0;
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+          if (lane + 32 * t < w) m = dmax(m, dmax(v.a[t], v.b[t]));
+        ans = warp_max(m);
+      } else {
+        if (p < 0.0) p = warp_max(v.a[0] < PST_INF ? v.a[0] : 0.0) * 0.25;
+        ans = warp_select<TM>(v, w, (int)a.k, p);
+      }
+      p = ans;
+      double ev = ans;
+      if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
+      if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
+      if (lane == jj) outv = sqrt(twol * ev);
+    }
+    if (lane < nj) Drow[jc + lane] = outv;
+    __syncwarp();  // chunk buffer is overwritten by the prefetch two chunks later
+  }
+}
+
+template <int P, int NT, int CHM>
 int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_mpdist<P, NT>;
+  auto kern = k_mpdist<P, NT, CHM>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
     pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -295,75 +672,162 @@ int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
   return PST_OK;
 }
 
+// P (columns per thread) is odd so the per-thread E[] stores are bank-conflict free.
+template <int TM>
+int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0) {
+  auto kern = k_select<TM>;
+  // per-warp chunk of JC windows (power of two <= 32), padded stride JC+1
+  int JC = 32;
+  while (JC > 2 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 150 * 1024) JC /= 2;
+  const size_t smem = smem0 + (size_t)16 * a.w * (JC + 1) * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return PST_ECUDA;
+    }
+  }
+  kern<<<grid, 256, smem, c->st2>>>(a, NCmax, JC);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int tm, int NCmax, size_t smem) {
+  if (tm <= 1) return launch_sel_t<1>(c, a, grid, NCmax, smem);
+  if (tm <= 2) return launch_sel_t<2>(c, a, grid, NCmax, smem);
+  if (tm <= 4) return launch_sel_t<4>(c, a, grid, NCmax, smem);
+  if (tm <= 9) return launch_sel_t<9>(c, a, grid, NCmax, smem);
+  if (tm <= 16) return launch_sel_t<16>(c, a, grid, NCmax, smem);
+  pst_set_error("window count w=%lld > 512 not supported by the selection kernel yet", (long long)a.w);
+  return PST_EINVAL;
+}
+
 template <int NT>
-int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, size_t smem) {
+int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, int chm, size_t smem) {
+  if (chm == 3) return P == 5 ? launch_p<5, NT, 3>(c, a, grid, smem) : launch_p<7, NT, 3>(c, a, grid, smem);
+  if (chm == 5) return P == 5 ? launch_p<5, NT, 5>(c, a, grid, smem) : launch_p<7, NT, 5>(c, a, grid, smem);
+  if (chm == 9) return P == 5 ? launch_p<5, NT, 9>(c, a, grid, smem) : launch_p<7, NT, 9>(c, a, grid, smem);
   switch (P) {
-    case 8: return launch_p<8, NT>(c, a, grid, smem);
-    case 7: return launch_p<7, NT>(c, a, grid, smem);
-    case 6: return launch_p<6, NT>(c, a, grid, smem);
-    case 5: return launch_p<5, NT>(c, a, grid, smem);
-    case 4: return launch_p<4, NT>(c, a, grid, smem);
-    case 3: return launch_p<3, NT>(c, a, grid, smem);
-    case 2: return launch_p<2, NT>(c, a, grid, smem);
-    default: return launch_p<1, NT>(c, a, grid, smem);
+    case 9: return launch_p<9, NT, 0>(c, a, grid, smem);
+    case 7: return launch_p<7, NT, 0>(c, a, grid, smem);
+    case 5: return launch_p<5, NT, 0>(c, a, grid, smem);
+    case 3: return launch_p<3, NT, 0>(c, a, grid, smem);
+    default: return launch_p<1, NT, 0>(c, a, grid, smem);
   }
 }
 
 }  // namespace
 
 // Profiles of segments [seg_lo, seg_hi) into D_dev rows 0.. (row stride ld).
+static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                              double* D_dev, int64_t ld);
+
 int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
                   double* D_dev, int64_t ld) {
   PST_TRY(pst_ensure_len(c, l));
+  if (!c->timing) return launch_mpdist_impl(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  cudaEvent_t e0, e1;
+  PST_CUDA(cudaEventCreate(&e0));
+  PST_CUDA(cudaEventCreate(&e1));
+  PST_CUDA(cudaEventRecord(e0, c->st));
+  const int64_t before = c->launches;
+  int r = launch_mpdist_impl(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  PST_CUDA(cudaEventRecord(e1, c->st));
+  if (!c->tev) c->tev = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
+  ((std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev)->push_back({e0, e1});
+  c->t_launch += c->launches - before;
+  return r;
+}
+
+static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                              double* D_dev, int64_t ld) {
   const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
   // tile geometry: NC = NT*P columns, T = NC - w + 1 windows; aim for T >= 4w
-  int P = 8, nt = (5 * w > 256 * 8) ? 512 : 256;
+  int nt = (4 * w > 256 * 5) ? 512 : 256;
+  int P = 5;
+  // register van Herk for w <= 32*9; chunk width class
+  const int chm = (w <= 96) ? 3 : (w <= 160) ? 5 : (w <= 288) ? 9 : 0;
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
-    return (size_t)(l + w + 3 * (int64_t)tt * pp + 64 + 2) * sizeof(double);
+    const int64_t ncm = (int64_t)tt * pp;
+    return (size_t)(l + 4 * w + ncm * (chm ? 2 : 4) + 64 + 2 + (tt / 32) * 32 * (chm ? chm : 1)) * sizeof(double);
   };
-  while (P > 1 && smem_for(P, nt) > smax) P--;
+  while (P > 1 && smem_for(P, nt) > smax) P -= 2;
   if (smem_for(P, nt) > smax || (int64_t)nt * P < w) {
     pst_set_error("snippet size %lld too large for shared-memory tiles", (long long)m);
     return PST_EINVAL;
   }
   const int64_t NCmax = (int64_t)nt * P;
   int64_t T = NCmax - w + 1;
+  if (T >= 2 * w) T = (T / w) * w;  // whole van Herk blocks: balanced warps, no partial block
   if (T > N) T = N;
   if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < T) T = v; }
   const int64_t ntile = (N + T - 1) / T;
-  // scratch: w*T doubles per CTA; bound CTAs per launch by the scratch budget
-  const size_t per_cta = (size_t)w * (size_t)T * sizeof(double);
-  size_t budget = (size_t)4 << 30;
+  // scratch: AB (S*T doubles) + allP_BA (NCmax doubles) per CTA, two buffers so the
+  // selection of batch b (stream st2) overlaps the row loop of batch b+1 (stream st).
+  const size_t ab_cta = (size_t)w * (size_t)T * sizeof(double);
+  const size_t per_cta = ab_cta + (size_t)NCmax * sizeof(double);
+  size_t budget = (size_t)6 << 30;
   {
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 4 + c->scratch_bytes);
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 3 + c->scratch_bytes);
   }
-  int64_t segs_per = (int64_t)(budget / (per_cta * (size_t)ntile));
+  int64_t segs_per = (int64_t)(budget / 2 / (per_cta * (size_t)ntile));
   if (segs_per < 1) segs_per = 1;
   if (segs_per > 65535) segs_per = 65535;
-  if (segs_per > seg_hi - seg_lo) segs_per = seg_hi - seg_lo;
-  PST_TRY(pst_ensure((void**)&c->scratch, &c->scratch_bytes, per_cta * (size_t)ntile * (size_t)segs_per));
+  const int64_t nseg = seg_hi - seg_lo;
+  if (nseg > 1 && segs_per >= nseg) segs_per = (nseg + 1) / 2;  // at least two batches to overlap
+  if (segs_per > nseg) segs_per = nseg;
+  const size_t buf_bytes = per_cta * (size_t)ntile * (size_t)segs_per;
+  PST_TRY(pst_ensure((void**)&c->scratch, &c->scratch_bytes, 2 * buf_bytes));
+  if (!c->st2) {
+    PST_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    for (int bi = 0; bi < 2; ++bi) {
+      PST_CUDA(cudaEventCreateWithFlags(&c->ev_rows[bi], cudaEventDisableTiming));
+      PST_CUDA(cudaEventCreateWithFlags(&c->ev_sel[bi], cudaEventDisableTiming));
+    }
+  }
   MPArgs a;
   a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
   a.df = c->L.df; a.dg = c->L.dg;
   a.n = n; a.l = l; a.m = m; a.w = w; a.k = k; a.Nl = Nl; a.N = N; a.T = T;
-  a.D = D_dev; a.ldD = ld; a.ab = c->scratch;
+  a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
+  a.dbg_nostore = getenv("PASTILA_NOSTORE") ? 1 : 0;
   if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));
     a.dbg_ba = c->dbg;
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
   }
-  if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < T) T = v; a.T = T; }
   const size_t smem = smem_for(P, nt);
-  for (int64_t s0 = seg_lo; s0 < seg_hi; s0 += segs_per) {
+  const int tm = (int)((w + 31) >> 5);
+  const size_t smem_sel = (size_t)NCmax * sizeof(double);
+  // the selection stream starts after everything queued before on the main stream
+  PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
+  PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[1], 0));
+  PST_CUDA(cudaEventRecord(c->ev_sel[0], c->st2));
+  PST_CUDA(cudaEventRecord(c->ev_sel[1], c->st2));
+  int bi = 0;
+  for (int64_t s0 = seg_lo; s0 < seg_hi; s0 += segs_per, bi ^= 1) {
     const int64_t ns = std::min(segs_per, seg_hi - s0);
     a.seg0 = s0;
     a.rowD0 = s0 - seg_lo;
+    char* buf = (char*)c->scratch + bi * buf_bytes;
+    a.ab = (double*)buf;
+    a.ba = (double*)(buf + ab_cta * (size_t)ntile * (size_t)segs_per);
     dim3 grid((unsigned)ntile, (unsigned)ns);
-    int r = (nt == 512) ? launch_nt<512>(c, a, grid, P, smem) : launch_nt<256>(c, a, grid, P, smem);
+    PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[bi], 0));  // buffer bi free again
+    int r = (nt == 512) ? launch_nt<512>(c, a, grid, P, chm, smem) : launch_nt<256>(c, a, grid, P, chm, smem);
     if (r != PST_OK) return r;
+    PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
+    PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));
+    r = launch_sel(c, a, grid, tm, (int)NCmax, smem_sel);
+    if (r != PST_OK) return r;
+    PST_CUDA(cudaEventRecord(c->ev_sel[bi], c->st2));
   }
+  // the main stream continues only after all selections
+  PST_CUDA(cudaEventRecord(c->ev_sel[0], c->st2));
+  PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[0], 0));
   return PST_OK;
 }

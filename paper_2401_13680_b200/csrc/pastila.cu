@@ -483,6 +483,14 @@ int pst_destroy(pst_ctx* c) {
                   c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    for (int bi = 0; bi < 2; ++bi) {
+      cudaEventDestroy(c->ev_rows[bi]);
+      cudaEventDestroy(c->ev_sel[bi]);
+    }
+    cudaStreamDestroy(c->st2);
+  }
   cudaStreamDestroy(c->st);
   delete c;
   return PST_OK;
@@ -852,6 +860,52 @@ int pst_labels(pst_ctx* c, const double* P, int64_t K, int64_t N, int64_t n, int
   PST_CUDA(cudaGetLastError());
   PST_CUDA(cudaMemcpyAsync(labels, dl, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// The context's CUDA stream (cudaStream_t), for event timing by callers.
+int pst_stream(pst_ctx* c, void** out) {
+  if (!valid(c)) return PST_EINVAL;
+  *out = (void*)c->st;
+  return PST_OK;
+}
+
+// Profile-kernel timing: enable(1)/disable(0) and reset; read accumulated
+// device milliseconds and kernel launches of all profile computations since.
+int pst_timing(pst_ctx* c, int enable) {
+  if (!valid(c)) return PST_EINVAL;
+  c->timing = enable != 0;
+  c->t_ms = 0.0;
+  c->t_calls = 0;
+  c->t_launch = 0;
+  if (c->tev) {
+    auto* v = (std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev;
+    for (auto& p : *v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    v->clear();
+  }
+  return PST_OK;
+}
+
+int pst_timing_read(pst_ctx* c, double* ms, int64_t* launches) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  if (c->tev) {
+    auto* v = (std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev;
+    for (auto& p : *v) {
+      float f = 0.f;
+      PST_CUDA(cudaEventElapsedTime(&f, p.first, p.second));
+      c->t_ms += f;
+      c->t_calls++;
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    v->clear();
+  }
+  *ms = c->t_ms;
+  *launches = c->t_launch;
   return PST_OK;
 }
 

@@ -1,0 +1,69 @@
+"""Attribute ncu SASS-level samples / executed instructions to CUDA source lines.
+
+usage: python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> [top]
+Needs the .so compiled with -lineinfo (it is) and nvdisasm/cuobjdump in PATH.
+"""
+import csv, io, re, subprocess, sys, collections, tempfile, os
+
+rep, kre = sys.argv[1], sys.argv[2]
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2401_13680_b200", "libpastila.so")
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+kname = rows[0][1]
+hdr = rows[1]
+ia, isrc = hdr.index("Address"), hdr.index("Source")
+iw = hdr.index("Warp Stall Sampling (All Samples)")
+ie = hdr.index("Instructions Executed")
+sass = []
+for r in rows[2:]:
+    try:
+        sass.append((int(r[ia], 16), int(r[iw] or 0), int(r[ie] or 0), r[isrc]))
+    except Exception:
+        pass
+# line info from nvdisasm of the matching function
+tmp = tempfile.mkdtemp()
+subprocess.run(["cuobjdump", "-xelf", "all", so], cwd=tmp, capture_output=True)
+cubins = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")]
+addr2line = {}
+mang = None
+for cb in cubins:
+    txt = subprocess.run(["nvdisasm", "-g", "-c", cb], capture_output=True, text=True).stdout
+    cur = None; line = None
+    for ln in txt.splitlines():
+        m = re.match(r"\s*\.text\.(\S+):", ln)
+        if m:
+            cur = m.group(1)
+            continue
+        m = re.search(r"//## File \"([^\"]+)\", line (\d+)", ln)
+        if m:
+            line = (os.path.basename(m.group(1)), int(m.group(2)))
+            continue
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if m and cur and re.search(kre, cur):
+            addr2line[(cur, int(m.group(1), 16))] = line
+funcs = sorted({f for f, _ in addr2line})
+# pick the function whose instruction count matches
+best = None
+for f in funcs:
+    n = sum(1 for (ff, _) in addr2line if ff == f)
+    if best is None or abs(n - len(sass)) < abs(best[1] - len(sass)):
+        best = (f, n)
+f = best[0]
+agg = collections.defaultdict(lambda: [0, 0])
+tot_w = sum(s[1] for s in sass) or 1
+tot_e = sum(s[2] for s in sass) or 1
+base = sass[0][0]
+for i, (a, w, e, src) in enumerate(sass):
+    key = addr2line.get((f, a - base), ("?", -1))
+    agg[key][0] += w
+    agg[key][1] += e
+print(f"kernel {kname}  ({len(sass)} SASS instrs; function {f})")
+srcfile = {}
+for (fn, ln), (w, e) in sorted(agg.items(), key=lambda t: -t[1][0])[:top]:
+    if fn not in srcfile:
+        p = os.path.join(os.path.dirname(so), "csrc", fn)
+        srcfile[fn] = open(p).read().splitlines() if os.path.exists(p) else []
+    text = srcfile[fn][ln - 1].strip() if 0 < ln <= len(srcfile[fn]) else ""
+    print(f"{100*w/tot_w:5.1f}% stall {100*e/tot_e:5.1f}% inst  {fn}:{ln:<4d} {text[:90]}")

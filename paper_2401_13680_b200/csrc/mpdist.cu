@@ -57,16 +57,30 @@ __device__ __forceinline__ unsigned dlo(double v) { return (unsigned)__double_as
 __device__ __forceinline__ double dmk(unsigned hi, unsigned lo) {
   return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
 }
-// exact warp max / min of non-negative doubles via two 32-bit REDUX steps
+// exact warp max / min of doubles via two 32-bit REDUX steps on the
+// order-preserving 64-bit key (sign-flipped bit pattern): tiny negative
+// rounding residues of e = 1 - rho order correctly.
+__device__ __forceinline__ unsigned long long okey(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ukey(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
 __device__ __forceinline__ double warp_max(double v) {
-  const unsigned h = __reduce_max_sync(FULLMASK, dhi(v));
-  const unsigned l = __reduce_max_sync(FULLMASK, dhi(v) == h ? dlo(v) : 0u);
-  return dmk(h, l);
+  const unsigned long long k = okey(v);
+  const unsigned kh = (unsigned)(k >> 32), kl = (unsigned)k;
+  const unsigned h = __reduce_max_sync(FULLMASK, kh);
+  const unsigned l = __reduce_max_sync(FULLMASK, kh == h ? kl : 0u);
+  return ukey(((unsigned long long)h << 32) | l);
 }
 __device__ __forceinline__ double warp_min(double v) {
-  const unsigned h = __reduce_min_sync(FULLMASK, dhi(v));
-  const unsigned l = __reduce_min_sync(FULLMASK, dhi(v) == h ? dlo(v) : 0xffffffffu);
-  return dmk(h, l);
+  const unsigned long long k = okey(v);
+  const unsigned kh = (unsigned)(k >> 32), kl = (unsigned)k;
+  const unsigned h = __reduce_min_sync(FULLMASK, kh);
+  const unsigned l = __reduce_min_sync(FULLMASK, kh == h ? kl : 0xffffffffu);
+  return ukey(((unsigned long long)h << 32) | l);
 }
 
 template <int TM>
@@ -86,12 +100,12 @@ __device__ __forceinline__ void count2(const WinVals<TM>& v, double p, int& lt, 
   le = __reduce_add_sync(FULLMASK, l2);
 }
 template <int TM>
-__device__ __forceinline__ double below_max(const WinVals<TM>& v, double p) {  // largest element < p (or 0)
-  double m = 0.0;
+__device__ __forceinline__ double below_max(const WinVals<TM>& v, double p) {  // largest element < p (or -inf)
+  double m = -PST_INF;
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
-    m = dmax(m, v.a[t] < p ? v.a[t] : 0.0);
-    m = dmax(m, v.b[t] < p ? v.b[t] : 0.0);
+    m = dmax(m, v.a[t] < p ? v.a[t] : -PST_INF);
+    m = dmax(m, v.b[t] < p ? v.b[t] : -PST_INF);
   }
   return warp_max(m);
 }
@@ -109,7 +123,7 @@ __device__ __forceinline__ double above_min(const WinVals<TM>& v, double p) {  /
 // k-th smallest; p = pivot hint (any value >= 0).  2w > k assumed.
 template <int TM>
 __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
-  double lov = 0.0, hi = PST_INF;
+  double lov = -1.0, hi = PST_INF;
   int clo = 0, chi = 2 * w;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
@@ -196,65 +210,62 @@ __device__ void select_run(const double* __restrict__ ab, int S, const double* _
 //   AB[u] = min(SUF_b[u], PRE_{b+1}[u-1])
 // is done in registers (4 mins per element).  Writes clamped AB values to the
 // transposed scratch column of each window.
-template <int CHM>
-__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int NC, int NJ, int w, int CH, int LPB,
-                                           int warp, int lane, int nw, double* __restrict__ abrow,
-                                           double* __restrict__ stg) {
-  const int bpw = 32 / LPB;                 // blocks per warp
-  const int sub = lane / LPB, ll = lane % LPB;
-  const int nblk = (NJ + w - 1) / w;
-  for (int b0 = warp * bpw; b0 < nblk; b0 += nw * bpw) {  // warp-uniform trip count
-    const int b = b0 + sub;
-    const int bb = b * w, bn = bb + w;
-    const int u0 = ll * CH;
-    double sf[CHM], pr[CHM];
+struct VHGeom {
+  int LPB, bpw, sub, ll, nblk, u0;
+};
+
+// E holds +inf beyond the tile's last column (rows never read past NC + w).
+template <int CH>
+__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int NJ, int w, const VHGeom& g, int warp,
+                                           int lane, int nw, double* __restrict__ abrow, double* __restrict__ stg) {
+  for (int b0 = warp * g.bpw; b0 < g.nblk; b0 += nw * g.bpw) {  // warp-uniform trip count
+    const bool live = b0 + g.sub < g.nblk;  // lane group has a block this iteration
+    const int bb = (b0 + g.sub) * w, bn = bb + w;
+    double sf[CH], pr[CH];
     double run = PST_INF;
 #pragma unroll
-    for (int t = CHM - 1; t >= 0; --t) {
-      const int u = u0 + t;
-      const double v = (t < CH && u < w && bb + u < NC) ? E[bb + u] : PST_INF;
+    for (int t = CH - 1; t >= 0; --t) {
+      const int u = g.u0 + t;
+      const double v = (live && u < w) ? E[bb + u] : PST_INF;
       run = dmin(run, v);
       sf[t] = run;
     }
     double totS = run;
     run = PST_INF;
 #pragma unroll
-    for (int t = 0; t < CHM; ++t) {
-      const int u = u0 + t;
-      const double v = (t < CH && u < w && bn + u < NC) ? E[bn + u] : PST_INF;
+    for (int t = 0; t < CH; ++t) {
+      const int u = g.u0 + t;
+      const double v = (live && u < w) ? E[bn + u] : PST_INF;
       run = dmin(run, v);
       pr[t] = run;
     }
     double totP = run;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      if (off < LPB) {
-        const double ds = __shfl_down_sync(FULLMASK, totS, off, LPB);
-        const double dp = __shfl_up_sync(FULLMASK, totP, off, LPB);
+      if (off < g.LPB) {
+        const double ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
+        const double dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
         totS = dmin(totS, ds);
         totP = dmin(totP, dp);
       }
     }
-    double cs = __shfl_down_sync(FULLMASK, totS, 1, LPB);
-    double cp = __shfl_up_sync(FULLMASK, totP, 1, LPB);
-    if (ll == LPB - 1) cs = PST_INF;
-    if (ll == 0) cp = PST_INF;
+    double cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
+    double cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
+    if (g.ll == g.LPB - 1) cs = PST_INF;
+    if (g.ll == 0) cp = PST_INF;
     const double C = dmin(cs, cp);
-    // combine into the warp's staging row (window offsets (b-b0)*w + u) ...
+    double* st = stg + g.sub * w;
 #pragma unroll
-    for (int t = 0; t < CHM; ++t) {
-      const int u = u0 + t;
-      if (t < CH && u < w) {
-        double v = dmin(sf[t], C);
-        if (t > 0) v = dmin(v, pr[t - 1]);
-        stg[sub * w + u] = clamp0(v);
-      }
+    for (int t = 0; t < CH; ++t) {
+      const int u = g.u0 + t;
+      if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
     }
     __syncwarp();
-    // ... then one coalesced row-major store of the warp's bpw*w windows
     const int jb = b0 * w;
-    const int cnt = min(bpw * w, NJ - jb);
-    for (int idx = lane; idx < cnt; idx += 32) abrow[jb + idx] = stg[idx];
+    const int cnt = min(g.bpw * w, NJ - jb);
+    double* dst = abrow + jb;
+#pragma unroll 4
+    for (int idx = lane; idx < cnt; idx += 32) dst[idx] = stg[idx];
     __syncwarp();
   }
 }
@@ -301,7 +312,7 @@ __device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double
     for (int u = lane; u < w && bb + u < NJ; u += 32) {
       double v = SUF[bb + u];
       if (u > 0) v = dmin(v, PRE[bn + u - 1]);
-      abrow[bb + u] = clamp0(v);
+      abrow[bb + u] = v;
     }
   }
 }
@@ -405,12 +416,19 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
   __syncthreads();
 
   const int qloc = (int)(q0 - J0) - tid * P;  // my local index of the self column at row 0
-  const int CH = (CHM > 0) ? (((w + 31) / 32) | 1) : 0;
-  int LPB = 32;
-  if (CHM > 0) {
-    while (LPB > 8 && (LPB / 2) * CHM >= w && (((w + LPB / 2 - 1) / (LPB / 2)) | 1) <= CHM) LPB /= 2;
+  VHGeom g;
+  {
+    int LPB = 1;
+    while (LPB < 32 && LPB * (CHM > 0 ? CHM : 1) < w) LPB *= 2;
+    if (LPB < 8) LPB = 8;
+    g.LPB = LPB;
+    g.bpw = 32 / LPB;
+    g.sub = lane / LPB;
+    g.ll = lane % LPB;
+    g.nblk = (NJ + w - 1) / w;
+    g.u0 = g.ll * (CHM > 0 ? CHM : 1);
   }
-  const int CHr = (CHM > 0) ? ((((w + LPB - 1) / LPB)) | 1) : 0;
+  const bool tail = (tid + 1) * P > NC;  // this thread owns columns past the tile's last one
   for (int i = 0; i < w; ++i) {
     double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
     if (i > 0) {
@@ -432,6 +450,11 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
         colmin[p] = dmin(colmin[p], e);
         Et[p] = e;
       }
+      if (tail) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          if (tid * P + p >= NC) Et[p] = PST_INF;
+      }
     } else {  // constant query window (row-uniform branch): zdist.py:111-112
 #pragma unroll
       for (int p = 0; p < P; ++p) {
@@ -447,7 +470,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
     }
     __syncthreads();
     if constexpr (CHM > 0)
-      vh_row_reg<CHM>(E, NC, NJ, w, CHr, LPB, warp, lane, NW, ab + (int64_t)i * T, STG + warp * 32 * CHM);
+      vh_row_reg<CHM>(E, NJ, w, g, warp, lane, NW, ab + (int64_t)i * T, STG + warp * 32 * CHM);
     else {
       vh_row_smem(E, SUF, PRE, NC, NJ, w, warp, lane, NW, ab + (int64_t)i * T);
       __syncthreads();  // SUF/PRE reused next row
@@ -463,7 +486,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
   for (int p = 0; p < P; ++p) {
     const int cl = tid * P + p;
     const int64_t c = J0 + cl;
-    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : clamp0(colmin[p]);
+    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : colmin[p];
   }
   __syncthreads();
   {
@@ -582,7 +605,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 template <int TM>
-__global__ void __launch_bounds__(256) k_select(const MPArgs a, int NCmax, int JC) {
+__global__ void __launch_bounds__(256, 1) k_select(const MPArgs a, int NCmax, int JC) {
   extern __shared__ double smb[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = (int)a.w, T = (int)a.T;
@@ -629,22 +652,23 @@ __global__ void __launch_bounds__(256) k_select(const MPArgs a, int NCmax, int J
       const int j = jc + jj;
       const double* Bw = BA + j;
       WinVals<TM> v;
+      const double* ca = chunk + lane * SJ + jj;
+      const double* cb = Bw + lane;
 #pragma unroll
       for (int t = 0; t < TM; ++t) {
-        const int idx = lane + 32 * t;
-        const bool ok = idx < w;
-        v.a[t] = ok ? chunk[idx * SJ + jj] : PST_INF;
-        v.b[t] = ok ? Bw[idx] : PST_INF;
+        const bool ok = lane + 32 * t < w;
+        v.a[t] = ok ? ca[32 * t * SJ] : PST_INF;
+        v.b[t] = ok ? cb[32 * t] : PST_INF;
       }
       double ans;
       if (2 * w <= (int)a.k) {
-        double m = 0.0;
+        double m = -PST_INF;
 #pragma unroll
         for (int t = 0; t < TM; ++t)
           if (lane + 32 * t < w) m = dmax(m, dmax(v.a[t], v.b[t]));
         ans = warp_max(m);
       } else {
-        if (p < 0.0) p = warp_max(v.a[0] < PST_INF ? v.a[0] : 0.0) * 0.25;
+        if (p < 0.0) p = dmax(warp_max(v.a[0] < PST_INF ? v.a[0] : -PST_INF) * 0.25, 0.0);
         ans = warp_select<TM>(v, w, (int)a.k, p);
       }
       p = ans;
@@ -694,10 +718,19 @@ int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0
 }
 
 int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int tm, int NCmax, size_t smem) {
-  if (tm <= 1) return launch_sel_t<1>(c, a, grid, NCmax, smem);
-  if (tm <= 2) return launch_sel_t<2>(c, a, grid, NCmax, smem);
-  if (tm <= 4) return launch_sel_t<4>(c, a, grid, NCmax, smem);
-  if (tm <= 9) return launch_sel_t<9>(c, a, grid, NCmax, smem);
+  switch (tm) {
+    case 1: return launch_sel_t<1>(c, a, grid, NCmax, smem);
+    case 2: return launch_sel_t<2>(c, a, grid, NCmax, smem);
+    case 3: return launch_sel_t<3>(c, a, grid, NCmax, smem);
+    case 4: return launch_sel_t<4>(c, a, grid, NCmax, smem);
+    case 5: return launch_sel_t<5>(c, a, grid, NCmax, smem);
+    case 6: return launch_sel_t<6>(c, a, grid, NCmax, smem);
+    case 7: return launch_sel_t<7>(c, a, grid, NCmax, smem);
+    case 8: return launch_sel_t<8>(c, a, grid, NCmax, smem);
+    case 9: return launch_sel_t<9>(c, a, grid, NCmax, smem);
+    default: break;
+  }
+  if (tm <= 12) return launch_sel_t<12>(c, a, grid, NCmax, smem);
   if (tm <= 16) return launch_sel_t<16>(c, a, grid, NCmax, smem);
   pst_set_error("window count w=%lld > 512 not supported by the selection kernel yet", (long long)a.w);
   return PST_EINVAL;
@@ -747,7 +780,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   int nt = (4 * w > 256 * 5) ? 512 : 256;
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class
-  const int chm = (w <= 96) ? 3 : (w <= 160) ? 5 : (w <= 288) ? 9 : 0;
+  const int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 288) ? 9 : 0;
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
     const int64_t ncm = (int64_t)tt * pp;

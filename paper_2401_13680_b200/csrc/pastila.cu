@@ -41,38 +41,54 @@ namespace {
 // ----------------------------------------------------------------- kernels
 // Exact sequential prefix sums (np.cumsum order, series.py:177-178) and the
 // running count of value changes (constant-window test, series.py:183-187).
-__global__ void k_prefix(const double* __restrict__ x, int64_t n, double* csum, double* csq, int64_t* chg) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0.0, q = 0.0;
+// The summation order must be strictly sequential to be bit-identical with
+// numpy, so one thread runs the dependent DADD chain; the other threads stage
+// chunks of x into shared memory (double-buffered, coalesced) and write the
+// results back, keeping global-memory latency off the chain.
+constexpr int PFX_CH = 1024;
+__global__ void __launch_bounds__(256) k_prefix(const double* __restrict__ x, int64_t n, double* csum, double* csq,
+                                                int64_t* chg) {
+  __shared__ double xin[2][PFX_CH];
+  __shared__ double os[PFX_CH], oq[PFX_CH];
+  __shared__ int64_t oc[PFX_CH];
+  const int tid = threadIdx.x;
+  double s = 0.0, q = 0.0, prev = 0.0;
   int64_t c = 0;
-  csum[0] = 0.0;
-  csq[0] = 0.0;
-  double prev = x[0];
-  int64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = x[i + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      s = __dadd_rn(s, v[u]);
-      q = __dadd_rn(q, __dmul_rn(v[u], v[u]));
-      if (i + u > 0 && v[u] != prev) ++c;
-      prev = v[u];
-      csum[i + u + 1] = s;
-      csq[i + u + 1] = q;
-      chg[i + u] = c;
-    }
+  if (tid == 0) {
+    csum[0] = 0.0;
+    csq[0] = 0.0;
   }
-  for (; i < n; ++i) {
-    const double v = x[i];
-    s = __dadd_rn(s, v);
-    q = __dadd_rn(q, __dmul_rn(v, v));
-    if (i > 0 && v != prev) ++c;
-    prev = v;
-    csum[i + 1] = s;
-    csq[i + 1] = q;
-    chg[i] = c;
+  const int64_t nch = (n + PFX_CH - 1) / PFX_CH;
+  for (int i = tid; i < PFX_CH && i < n; i += 256) xin[0][i] = x[i];
+  __syncthreads();
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int cur = (int)(ch & 1);
+    const int64_t base = ch * PFX_CH;
+    const int cnt = (int)min((int64_t)PFX_CH, n - base);
+    if (tid == 0) {
+      const double* xv = xin[cur];
+      for (int i = 0; i < cnt; ++i) {
+        const double v = xv[i];
+        s = __dadd_rn(s, v);
+        q = __dadd_rn(q, __dmul_rn(v, v));
+        if (base + i > 0 && v != prev) ++c;
+        prev = v;
+        os[i] = s;
+        oq[i] = q;
+        oc[i] = c;
+      }
+    } else if (ch + 1 < nch) {  // prefetch the next chunk meanwhile
+      const int64_t nb = base + PFX_CH;
+      const int ncnt = (int)min((int64_t)PFX_CH, n - nb);
+      for (int i = tid - 1; i < ncnt; i += 255) xin[cur ^ 1][i] = x[nb + i];
+    }
+    __syncthreads();
+    for (int i = tid; i < cnt; i += 256) {
+      csum[base + i + 1] = os[i];
+      csq[base + i + 1] = oq[i];
+      chg[base + i] = oc[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -523,7 +539,7 @@ static int set_series_common(pst_ctx* c, const double* x, int64_t n, cudaMemcpyK
   PST_CUDA(cudaMemcpyAsync(c->x, x, (size_t)n * sizeof(double), kind, c->st));
   c->n = n;
   c->L.l = -1;
-  k_prefix<<<1, 32, 0, c->st>>>(c->x, n, c->csum, c->csq, c->chg);
+  k_prefix<<<1, 256, 0, c->st>>>(c->x, n, c->csum, c->csq, c->chg);
   c->launches++;
   PST_CUDA(cudaGetLastError());
   return PST_OK;

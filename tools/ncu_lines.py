@@ -8,8 +8,8 @@ import csv, io, re, subprocess, sys, collections, tempfile, os
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2401_13680_b200", "libpastila.so")
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "-c", "1", "--page", "source", "--csv",
+                      "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 kname = rows[0][1]
 hdr = rows[1]
@@ -44,9 +44,12 @@ for cb in cubins:
         if m and cur and re.search(kre, cur):
             addr2line[(cur, int(m.group(1), 16))] = line
 funcs = sorted({f for f, _ in addr2line})
-# pick the function whose instruction count matches
+# match the template arguments of the profiled kernel, e.g. "<(int)5, (int)256, (int)5>"
+targs = re.findall(r"\(int\)(-?\d+)", kname)
+want = "".join(f"Li{v}E" for v in targs)
+cands = [f for f in funcs if want and want in f] or funcs
 best = None
-for f in funcs:
+for f in cands:
     n = sum(1 for (ff, _) in addr2line if ff == f)
     if best is None or abs(n - len(sass)) < abs(best[1] - len(sass)):
         best = (f, n)

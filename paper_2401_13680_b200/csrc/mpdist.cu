@@ -701,8 +701,10 @@ template <int TM>
 int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0) {
   auto kern = k_select<TM>;
   // per-warp chunk of JC windows (power of two <= 32), padded stride JC+1
+  // chunk width: small enough for >= 4 CTAs (32 warps) per SM -- the per-window
+  // work is a latency chain, so occupancy matters more than chunk length
   int JC = 32;
-  while (JC > 2 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 150 * 1024) JC /= 2;
+  while (JC > 2 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 52 * 1024) JC /= 2;
   const size_t smem = smem0 + (size_t)16 * a.w * (JC + 1) * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -793,7 +795,17 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   }
   const int64_t NCmax = (int64_t)nt * P;
   int64_t T = NCmax - w + 1;
-  if (T >= 2 * w) T = (T / w) * w;  // whole van Herk blocks: balanced warps, no partial block
+  if (T >= 2 * w) {
+    // whole van Herk blocks; prefer a multiple of the block slots per row (warps x
+    // lane groups) so every warp has the same number of blocks
+    int lpb = 1;
+    const int chv = chm ? chm : 1;
+    while (lpb < 32 && lpb * chv < w) lpb *= 2;
+    if (lpb < 8) lpb = 8;
+    const int64_t slots = (int64_t)(nt / 32) * (32 / lpb);
+    const int64_t nb = T / w;
+    T = (nb >= slots ? (nb / slots) * slots : nb) * w;
+  }
   if (T > N) T = N;
   if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < T) T = v; }
   const int64_t ntile = (N + T - 1) / T;

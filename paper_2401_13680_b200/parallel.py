@@ -84,21 +84,24 @@ def segment_ranges(S: int, parts: int):
 
 
 class ShardedSearch:
-    """Greedy snippet selection over segment rows split across ranks.
+    """Greedy snippet selection over segment rows split across ranks (one length).
 
-    ``backend`` provides the local (per-rank) device work:
-      areas(curve|None) -> float64[n_local]   row sums of min(D, curve)
-      row(i_local) -> float64[N]              one profile row
-      colmin() -> (float64[N], int64[N])      per-window min and local first argmin
-      rowmax() -> float                       max of the local rows
-    and ``to_tensor`` / ``from_tensor`` move arrays to the collective device.
+    ``backend`` provides the rank-local work on its rows [seg_lo, seg_hi):
+      areas(curve | None) -> float64[n_local]   row sums of min(D, curve)
+      row(i_local) -> float64[N]                one profile row
+      colmin() -> (float64[N], int64[N])        per-window min, local first argmin
+      rowmax() -> float                         max over the local rows
+    ``to_dev`` / ``from_dev`` move numpy arrays to / from the collective's device
+    (CUDA tensors under NCCL, CPU tensors under gloo).
     """
 
-    def __init__(self, backend, seg_lo: int, seg_hi: int, N: int, to_tensor, from_tensor):
+    def __init__(self, backend, ranges, N: int, to_dev, from_dev):
         self.b = backend
-        self.lo, self.hi, self.N = seg_lo, seg_hi, N
-        self.T = to_tensor
-        self.F = from_tensor
+        self.ranges = list(ranges)
+        self.lo, self.hi = self.ranges[rank()]
+        self.N = N
+        self.to_dev = to_dev
+        self.from_dev = from_dev
 
     def run(self, K: int):
         import torch
@@ -106,47 +109,98 @@ class ShardedSearch:
         dist = _dist()
         ws = world_size()
         chosen: list[int] = []
-        taken = set()
         curve = None
         for _ in range(K):
-            areas = self.b.areas(curve)
+            # local best (lowest index among equal areas), then global (area, index) minimum
+            areas = np.asarray(self.b.areas(curve), dtype=np.float64)
             best_a, best_i = np.inf, np.iinfo(np.int64).max
             for i, a in enumerate(areas):
                 g = self.lo + i
-                if g in taken:
+                if g in chosen:
                     continue
                 if a < best_a or (a == best_a and g < best_i):
-                    best_a, best_i = a, g
-            cand = torch.tensor([best_a, float(best_i)], dtype=torch.float64)
-            allc = [torch.zeros(2, dtype=torch.float64) for _ in range(ws)]
-            dist.all_gather(allc, self.T(cand))
-            pairs = [(float(self.F(c)[0]), int(self.F(c)[1])) for c in allc]
-            ga, gi = min(pairs, key=lambda p: (p[0], p[1]))
+                    best_a, best_i = float(a), g
+            cand = self.to_dev(np.array([best_a, float(best_i)]))
+            allc = [self.to_dev(np.zeros(2)) for _ in range(ws)]
+            dist.all_gather(allc, cand)
+            pairs = [tuple(self.from_dev(c)) for c in allc]
+            ga, gi = min(pairs, key=lambda t: (t[0], t[1]))
+            gi = int(gi)
             chosen.append(gi)
-            taken.add(gi)
-            owner = next(r for r in range(ws) if self._range(r)[0] <= gi < self._range(r)[1])
-            row = self.b.row(gi - self.lo) if self.lo <= gi < self.hi else np.zeros(self.N)
-            rt = self.T(torch.from_numpy(np.ascontiguousarray(row)))
+            owner = next(r for r, (lo, hi) in enumerate(self.ranges) if lo <= gi < hi)
+            row = self.b.row(gi - self.lo) if owner == rank() else np.zeros(self.N)
+            rt = self.to_dev(np.ascontiguousarray(row, dtype=np.float64))
             dist.broadcast(rt, src=owner)
-            row = self.F(rt)
+            row = self.from_dev(rt)
             curve = row.copy() if curve is None else np.minimum(curve, row)
         # nearest segment per window: MIN over values, then MIN over indices among ties
         mv, ma = self.b.colmin()
-        mvt = self.T(torch.from_numpy(np.ascontiguousarray(mv)))
+        mv = np.array(mv, dtype=np.float64, copy=True)
+        mvt = self.to_dev(mv.copy())  # reduced in place: keep the local minima
         dist.all_reduce(mvt, op=dist.ReduceOp.MIN)
-        gmin = self.F(mvt)
-        idx = np.where(mv == gmin, ma + self.lo, np.iinfo(np.int64).max).astype(np.int64)
-        it = self.T(torch.from_numpy(idx))
+        gmin = self.from_dev(mvt)
+        idx = np.where(mv == gmin, np.asarray(ma, dtype=np.int64) + self.lo, np.iinfo(np.int64).max)
+        it = self.to_dev(idx.astype(np.int64, copy=True))
         dist.all_reduce(it, op=dist.ReduceOp.MIN)
-        nearest = self.F(it)
-        pm = self.T(torch.tensor([self.b.rowmax()], dtype=torch.float64))
+        nearest = self.from_dev(it).astype(np.int64)
+        pm = self.to_dev(np.array([self.b.rowmax()], dtype=np.float64))
         dist.all_reduce(pm, op=dist.ReduceOp.MAX)
-        return chosen, curve, nearest, float(self.F(pm)[0])
+        return chosen, curve, nearest, float(self.from_dev(pm)[0])
 
-    def _range(self, r):
-        return self.ranges[r]
 
-    ranges: list = []
+class DeviceRows:
+    """ShardedSearch backend on this rank's GPU: the rank's segment profiles live
+    in a device matrix filled by the profile kernels (pst_profiles_dev); areas and
+    per-window minima run on the device (pst_areas_dev / pst_colmin_dev)."""
+
+    def __init__(self, series, params, seg_lo: int, seg_hi: int):
+        import ctypes as C
+
+        import torch
+
+        from . import _native
+
+        self.C = C
+        self.ctx = _native.context()
+        self.ctx.set_series(series.values)
+        self.dev = torch.device("cuda", self.ctx.device)
+        n, m = series.n, params.snippet_size
+        self.N = n - m + 1
+        self.rows = seg_hi - seg_lo
+        self.D = torch.empty((self.rows, self.N), dtype=torch.float64, device=self.dev)
+        self.ctx.call("pst_profiles_dev", int(m), int(params.window_size), int(params.k), int(seg_lo),
+                      int(seg_hi), C.c_void_p(self.D.data_ptr()), C.c_int64(self.N))
+        self.ctx.call("pst_sync")
+
+    def areas(self, curve):
+        import torch
+
+        out = torch.empty(self.rows, dtype=torch.float64, device=self.dev)
+        cptr = None
+        if curve is not None:
+            ct = torch.as_tensor(curve, dtype=torch.float64, device=self.dev)
+            cptr = self.C.c_void_p(ct.data_ptr())
+        self.ctx.call("pst_areas_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
+                      self.C.c_int64(self.N), self.C.c_int64(self.N), cptr, self.C.c_void_p(out.data_ptr()))
+        self.ctx.call("pst_sync")
+        return out.cpu().numpy()
+
+    def row(self, i):
+        return self.D[i].cpu().numpy()
+
+    def colmin(self):
+        import torch
+
+        mv = torch.empty(self.N, dtype=torch.float64, device=self.dev)
+        ma = torch.empty(self.N, dtype=torch.int32, device=self.dev)
+        self.ctx.call("pst_colmin_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
+                      self.C.c_int64(self.N), self.C.c_int64(self.N), self.C.c_int64(0),
+                      self.C.c_void_p(mv.data_ptr()), self.C.c_void_p(ma.data_ptr()))
+        self.ctx.call("pst_sync")
+        return mv.cpu().numpy(), ma.cpu().numpy().astype(np.int64)
+
+    def rowmax(self):
+        return float(self.D.max().item()) if self.rows else 0.0
 
 
 def timed(fn, *a, **kw):

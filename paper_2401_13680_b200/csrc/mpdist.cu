@@ -145,8 +145,8 @@ __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
     if (it < 2) {
       np = down ? hi : lov;  // adjacent-value step (rank moves of 1-2 are the common case)
     } else if (hi < PST_INF && it < 10) {
-      const double f = ((double)(k - clo) - 0.5) / (double)(chi - clo);
-      np = lov + (hi - lov) * f;
+      const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));  // heuristic pivot only
+      np = lov + (hi - lov) * (double)f;
     } else if (hi < PST_INF) {
       np = 0.5 * (lov + hi);
     } else {
@@ -157,51 +157,6 @@ __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
     p = np;
   }
   return p;
-}
-
-// Profiles for windows [j0, j1) of the tile: A columns at ab + j*S, B = BA + j.
-template <int TM>
-__device__ void select_run(const double* __restrict__ ab, int S, const double* __restrict__ BA, int w, int k, int j0,
-                           int j1, int lane, double* __restrict__ Drow, double twol) {
-  double p = -1.0;
-  double outv = 0.0;
-  for (int j = j0; j < j1; ++j) {
-    const double* A = ab + (int64_t)j * S;
-    const double* B = BA + j;
-    WinVals<TM> v;
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const int idx = lane + 32 * t;
-      const bool ok = idx < w;
-      v.a[t] = ok ? A[idx] : PST_INF;
-      v.b[t] = ok ? B[idx] : PST_INF;
-    }
-    double ans;
-    if (2 * w <= k) {  // max fallback (mpdist.py:230-231)
-      double m = 0.0;
-#pragma unroll
-      for (int t = 0; t < TM; ++t) {
-        const int idx = lane + 32 * t;
-        if (idx < w) m = dmax(m, dmax(v.a[t], v.b[t]));
-      }
-      ans = warp_max(m);
-    } else {
-      if (p < 0.0) {  // first window of the run: pivot at the median of lane 0..31's first A values
-        p = warp_max(v.a[0] < PST_INF ? v.a[0] : 0.0) * 0.25;
-      }
-      ans = warp_select<TM>(v, w, k, p);
-    }
-    p = ans;
-    double ev = ans;
-    if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
-    if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
-    const double dv = sqrt(twol * ev);
-    if (lane == ((j - j0) & 31)) outv = dv;
-    if (((j - j0) & 31) == 31 || j == j1 - 1) {  // flush up to 32 outputs with one coalesced store
-      const int base = j - ((j - j0) & 31);
-      if (base + lane <= j) Drow[base + lane] = outv;
-    }
-  }
 }
 
 // van Herk row sliding minima for one row, register version.
@@ -499,14 +454,15 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
 
 // Generic (memory-resident) variant of the warp selection for 2w > 32*2*16.
 struct MemWin {
-  const double* A;
-  const double* B;
+  const double* A;  // row minima, stride sa
+  const double* B;  // column minima, contiguous
   int w;
+  int64_t sa;
 };
 __device__ __forceinline__ void count2m(const MemWin& v, int lane, double p, int& lt, int& le) {
   int l1 = 0, l2 = 0;
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i], y = v.B[i];
+    const double x = v.A[i * v.sa], y = v.B[i];
     l1 += (x < p) + (y < p);
     l2 += (x <= p) + (y <= p);
   }
@@ -514,18 +470,18 @@ __device__ __forceinline__ void count2m(const MemWin& v, int lane, double p, int
   le = __reduce_add_sync(FULLMASK, l2);
 }
 __device__ __forceinline__ double below_maxm(const MemWin& v, int lane, double p) {
-  double m = 0.0;
+  double m = -PST_INF;
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i], y = v.B[i];
-    m = dmax(m, x < p ? x : 0.0);
-    m = dmax(m, y < p ? y : 0.0);
+    const double x = v.A[i * v.sa], y = v.B[i];
+    m = dmax(m, x < p ? x : -PST_INF);
+    m = dmax(m, y < p ? y : -PST_INF);
   }
   return warp_max(m);
 }
 __device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p) {
   double m = PST_INF;
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i], y = v.B[i];
+    const double x = v.A[i * v.sa], y = v.B[i];
     m = dmin(m, x > p ? x : PST_INF);
     m = dmin(m, y > p ? y : PST_INF);
   }
@@ -533,7 +489,7 @@ __device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p
 }
 __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
   const int w = v.w;
-  double lov = 0.0, hi = PST_INF;
+  double lov = -1.0, hi = PST_INF;
   int clo = 0, chi = 2 * w;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
@@ -555,8 +511,8 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
     if (it < 2) {
       np = down ? hi : lov;
     } else if (hi < PST_INF && it < 10) {
-      const double f = ((double)(k - clo) - 0.5) / (double)(chi - clo);
-      np = lov + (hi - lov) * f;
+      const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));  // heuristic pivot only
+      np = lov + (hi - lov) * (double)f;
     } else if (hi < PST_INF) {
       np = 0.5 * (lov + hi);
     } else {
@@ -567,28 +523,6 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
     p = np;
   }
   return p;
-}
-
-__device__ void select_run_mem(const double* __restrict__ ab, int S, const double* __restrict__ BA, int w, int k,
-                               int j0, int j1, int lane, double* __restrict__ Drow, double twol) {
-  double p = -1.0;
-  for (int j = j0; j < j1; ++j) {
-    MemWin v{ab + (int64_t)j * S, BA + j, w};
-    double ans;
-    if (2 * w <= k) {
-      double m = 0.0;
-      for (int i = lane; i < w; i += 32) m = dmax(m, dmax(v.A[i], v.B[i]));
-      ans = warp_max(m);
-    } else {
-      if (p < 0.0) p = warp_max(v.A[lane < w ? lane : 0]) * 0.25;
-      ans = warp_select_mem(v, lane, k, p);
-    }
-    p = ans;
-    double ev = ans;
-    if (ev < 1e-15) ev = 0.0;
-    if (ev > 2.0) ev = 2.0;
-    if (lane == 0) Drow[j] = sqrt(twol * ev);
-  }
 }
 
 // Selection kernel: one CTA per (tile, segment) of the row kernel's scratch.
@@ -672,13 +606,53 @@ __global__ void __launch_bounds__(256, 1) k_select(const MPArgs a, int NCmax, in
         ans = warp_select<TM>(v, w, (int)a.k, p);
       }
       p = ans;
-      double ev = ans;
+      if (lane == jj) outv = ans;
+    }
+    if (lane < nj) {
+      double ev = outv;
       if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
       if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
-      if (lane == jj) outv = sqrt(twol * ev);
+      Drow[jc + lane] = sqrt(twol * ev);
     }
-    if (lane < nj) Drow[jc + lane] = outv;
     __syncwarp();  // chunk buffer is overwritten by the prefetch two chunks later
+  }
+}
+
+// Selection for very long windows (2w > 1024 elements): column gathered straight
+// from the row-major AB scratch (stride T), passes re-read memory.
+__global__ void __launch_bounds__(256) k_select_big(const MPArgs a, int NCmax) {
+  extern __shared__ double smb[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = (int)a.w, T = (int)a.T;
+  const int64_t J0 = (int64_t)blockIdx.x * a.T;
+  const int NJ = (int)min(a.T, a.N - J0);
+  const int NC = NJ + w - 1;
+  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const double* ab = a.ab + cta * ((int64_t)w * T);
+  const double* bag = a.ba + cta * NCmax;
+  for (int c = tid; c < NC; c += 256) smb[c] = bag[c];
+  __syncthreads();
+  const double twol = 2.0 * (double)a.l;
+  double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
+  const int per = (NJ + 7) / 8;
+  const int j0 = min(NJ, warp * per), j1 = min(NJ, j0 + per);
+  double p = -1.0;
+  for (int j = j0; j < j1; ++j) {
+    MemWin v{ab + j, smb + j, w, (int64_t)T};
+    double ans;
+    if (2 * w <= (int)a.k) {
+      double m = -PST_INF;
+      for (int i = lane; i < w; i += 32) m = dmax(m, dmax(v.A[i * v.sa], v.B[i]));
+      ans = warp_max(m);
+    } else {
+      if (p < 0.0) p = dmax(warp_max(lane < w ? v.A[lane * v.sa] : -PST_INF) * 0.25, 0.0);
+      ans = warp_select_mem(v, lane, (int)a.k, p);
+    }
+    p = ans;
+    double ev = ans;
+    if (ev < 1e-15) ev = 0.0;
+    if (ev > 2.0) ev = 2.0;
+    if (lane == 0) Drow[j] = sqrt(twol * ev);
   }
 }
 
@@ -704,7 +678,7 @@ int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0
   // chunk width: small enough for >= 4 CTAs (32 warps) per SM -- the per-window
   // work is a latency chain, so occupancy matters more than chunk length
   int JC = 32;
-  while (JC > 2 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 52 * 1024) JC /= 2;
+  while (JC > 4 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 52 * 1024) JC /= 2;
   const size_t smem = smem0 + (size_t)16 * a.w * (JC + 1) * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -734,8 +708,19 @@ int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int tm, int NCmax, size_t
   }
   if (tm <= 12) return launch_sel_t<12>(c, a, grid, NCmax, smem);
   if (tm <= 16) return launch_sel_t<16>(c, a, grid, NCmax, smem);
-  pst_set_error("window count w=%lld > 512 not supported by the selection kernel yet", (long long)a.w);
-  return PST_EINVAL;
+  {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_select_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+        return PST_ECUDA;
+      }
+    }
+    k_select_big<<<grid, 256, smem, c->st2>>>(a, NCmax);
+    c->launches++;
+    PST_CUDA(cudaGetLastError());
+    return PST_OK;
+  }
 }
 
 template <int NT>

@@ -97,6 +97,31 @@ def test_mpdist_random_vs_oracle(seed):
         np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
 
 
+@pytest.mark.parametrize("m", [24, 48, 80, 96, 97, 160, 161, 288, 289, 600, 1100])
+def test_mpdist_window_classes_vs_oracle(m):
+    """Every register class boundary of the row / selection kernels and the
+    long-window paths (w > 288 shared-memory van Herk, w > 512 gather selection)."""
+    rng = np.random.default_rng(m)
+    n = max(6 * m, 1500)
+    x = np.cumsum(rng.standard_normal(n)) * 0.1 + np.sin(np.arange(n) * 2 * np.pi / 37)
+    params = P.MPdistParams(m)
+    st = O.sliding_stats(x, params.window_size)
+    for seg in (0, n // m - 1):
+        got = P.mpdist_profile(P.TimeSeries(x), seg, params).values
+        ref = O.mpdist_profile(x, seg, m, params.window_size, params.k, st)
+        np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
+
+
+def test_max_fallback_and_tiny_windows():
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(300)
+    for m, l, k in [(10, 5, 100), (8, 8, 1), (6, 1, 2), (12, 2, 3)]:
+        params = P.MPdistParams(m, l, k)
+        got = P.mpdist_profile(P.TimeSeries(x), 3, params).values
+        ref = O.mpdist_profile(x, 3, m, l, k)
+        np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
+
+
 def _check_result(res, doc, arrays, prefix):
     assert [s.index for s in res.snippets] == doc["indices"]
     assert [s.start for s in res.snippets] == doc["starts"]

@@ -93,7 +93,8 @@ struct MPArgs {
   int64_t seg0;      // segment of blockIdx.y == 0
   double* D;         // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y)
   int64_t ldD, rowD0;
-  double* ab;        // scratch, w*T doubles per CTA
+  double* ab;        // scratch, w*Tp doubles per CTA, lane-run order (see mpdist.cu)
+  int64_t R, Tp;     // lane-run length (odd) and AB row stride Tp = 32*R >= T
   double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
   double* ba;        // scratch: allP_BA per CTA (NCmax doubles)
   int dbg_nostore;   // debug: skip AB stores (timing experiments only)

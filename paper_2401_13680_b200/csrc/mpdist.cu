@@ -34,29 +34,10 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 
 // ---------------------------------------------------------------- selection
 // Exact k-th smallest (1-based) of the 2w-element P_ABBA multiset of one
-// window: A = w row minima (contiguous column of the AB scratch, global),
-// B = w column minima (shared memory).  All values are clamped >= 0.
+// window (mpdist.py:224-231): A = w row minima (AB scratch), B = w column
+// minima (shared memory).  Helpers for the warp-cooperative exact path used
+// for run starts and rare large rank moves (k_select_run below).
 //
-// Adjacent windows share almost all of their multiset, so the previous
-// window's answer is the first pivot: one counting pass settles ~75% of
-// windows; a second pass that tracks the two nearest values on the needed
-// side settles rank moves of 1-2 (~23%); larger moves fall back to bracketing
-// passes (interpolation, then bisection on the order-preserving bit pattern).
-// ---------------------------------------------------------------- selection
-// Warp-cooperative exact k-th smallest of each window's 2w-element P_ABBA
-// multiset.  A warp sweeps a run of consecutive windows; for window j, lane L
-// holds A[L+32t] (row minima: contiguous column of the AB scratch) and
-// B[L+32t] (column minima window, shared memory) in registers.  Every
-// decision is warp-uniform (no divergence between windows).  The previous
-// window's answer is the first pivot: one counting pass settles ~75% of
-// windows, one adjacent-value step settles rank moves of 1, a second step
-// moves of 2; larger moves (and the first window of a run) use rank
-// interpolation / bisection between exact brackets.
-__device__ __forceinline__ unsigned dhi(double v) { return (unsigned)(__double_as_longlong(v) >> 32); }
-__device__ __forceinline__ unsigned dlo(double v) { return (unsigned)__double_as_longlong(v); }
-__device__ __forceinline__ double dmk(unsigned hi, unsigned lo) {
-  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
-}
 // exact warp max / min of doubles via two 32-bit REDUX steps on the
 // order-preserving 64-bit key (sign-flipped bit pattern): tiny negative
 // rounding residues of e = 1 - rho order correctly.
@@ -121,13 +102,19 @@ __device__ __forceinline__ double above_min(const WinVals<TM>& v, double p) {  /
 }
 
 // k-th smallest; p = pivot hint (any value >= 0).  2w > k assumed.
+// lt0/le0 >= 0: the counts of p are already known (skip the first pass).
 template <int TM>
-__device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
+__device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int lt0 = -1, int le0 = -1) {
   double lov = -1.0, hi = PST_INF;
   int clo = 0, chi = 2 * w;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
-    count2<TM>(v, p, lt, le);
+    if (it == 0 && lt0 >= 0) {
+      lt = lt0;
+      le = le0;
+    } else {
+      count2<TM>(v, p, lt, le);
+    }
     if (lt < k && k <= le) return p;
     bool down = k <= lt;
     if (down) {
@@ -163,16 +150,16 @@ __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p) {
 // Blocks of w columns; a group of LPB lanes owns block b (SUF) and block b+1
 // (PRE); lane chunks of CH (odd) consecutive columns; the combine
 //   AB[u] = min(SUF_b[u], PRE_{b+1}[u-1])
-// is done in registers (4 mins per element).  Writes clamped AB values to the
-// transposed scratch column of each window.
+// is done in registers (4 mins per element).  Results go to the CTA's row
+// buffer srow[j] (window j of the tile); store_ab_row moves it to HBM.
 struct VHGeom {
   int LPB, bpw, sub, ll, nblk, u0;
 };
 
 // E holds +inf beyond the tile's last column (rows never read past NC + w).
 template <int CH>
-__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int NJ, int w, const VHGeom& g, int warp,
-                                           int lane, int nw, double* __restrict__ abrow, double* __restrict__ stg) {
+__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, const VHGeom& g, int warp,
+                                           int nw, double* __restrict__ srow) {
   for (int b0 = warp * g.bpw; b0 < g.nblk; b0 += nw * g.bpw) {  // warp-uniform trip count
     const bool live = b0 + g.sub < g.nblk;  // lane group has a block this iteration
     const int bb = (b0 + g.sub) * w, bn = bb + w;
@@ -209,26 +196,34 @@ __device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int NJ,
     if (g.ll == g.LPB - 1) cs = PST_INF;
     if (g.ll == 0) cp = PST_INF;
     const double C = dmin(cs, cp);
-    double* st = stg + g.sub * w;
+    if (live) {
+      double* st = srow + bb;
 #pragma unroll
-    for (int t = 0; t < CH; ++t) {
-      const int u = g.u0 + t;
-      if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
+      for (int t = 0; t < CH; ++t) {
+        const int u = g.u0 + t;
+        if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
+      }
     }
-    __syncwarp();
-    const int jb = b0 * w;
-    const int cnt = min(g.bpw * w, NJ - jb);
-    double* dst = abrow + jb;
-#pragma unroll 4
-    for (int idx = lane; idx < cnt; idx += 32) dst[idx] = stg[idx];
-    __syncwarp();
+  }
+}
+
+// One AB row from the CTA row buffer to HBM in lane-run order: window
+// j = L*R + r (L = 0..31, r = 0..R-1) is stored at r*32 + L, so that the 32
+// lanes of a selection warp, which sweep windows L*R + r for r = 0, 1, ...,
+// read one contiguous 256-byte line per row.  Shared reads srow[L*R + r] have
+// odd stride R (bank-conflict free); global stores are contiguous.
+__device__ __forceinline__ void store_ab_row(const double* __restrict__ srow, double* __restrict__ dst, int NJ,
+                                             int R, int Tp, int tid, int nt) {
+  for (int pos = tid; pos < Tp; pos += nt) {
+    const int j = (pos & 31) * R + (pos >> 5);
+    if (j < NJ) dst[pos] = srow[j];
   }
 }
 
 // van Herk, shared-memory version for large w (chunks do not fit registers).
 __device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double* __restrict__ SUF,
                                             double* __restrict__ PRE, int NC, int NJ, int w, int warp, int lane,
-                                            int nw, double* __restrict__ abrow) {
+                                            int nw, double* __restrict__ srow) {
   const int nblk = (NJ + w - 1) / w;
   const int CH = (w + 31) / 32;
   for (int b = warp; b < nblk; b += nw) {
@@ -267,7 +262,7 @@ __device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double
     for (int u = lane; u < w && bb + u < NJ; u += 32) {
       double v = SUF[bb + u];
       if (u > 0) v = dmin(v, PRE[bn + u - 1]);
-      abrow[bb + u] = v;
+      srow[bb + u] = v;
     }
   }
 }
@@ -292,12 +287,14 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
   double* E1 = E0 + NCmax;     // [NCmax] row e-values (odd rows)
   double* xfer = E1 + NCmax;   // [64]
   double* red = xfer + 64;     // [2]
-  double* STG = red + 2;       // [NW * 32 * max(CHM,1)] per-warp staging of one AB row
-  double* SUF = STG + NW * 32 * (CHM > 0 ? CHM : 1);  // [NCmax] (shared-memory van Herk only)
-  double* PRE = SUF + NCmax;   // [NCmax]
+  double* SR0 = red + 2;        // [NCmax] AB row buffer (even rows)
+  double* SR1 = SR0 + NCmax;    // [NCmax] AB row buffer (odd rows)
+  double* SUF = SR1 + NCmax;    // [NCmax] (shared-memory van Herk only)
+  double* PRE = SUF + NCmax;    // [NCmax]
   double* E = E0;
-  // AB scratch of this CTA: row-major [w][T]
-  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * T);
+  // AB scratch of this CTA: [w][Tp], each row in lane-run order (store_ab_row)
+  const int R = (int)a.R, Tp = (int)a.Tp;
+  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
   const double* __restrict__ xJ = a.x + J0;
   const double* __restrict__ xQ = a.x + q0;
   const double* __restrict__ muJ = a.mu + J0;
@@ -424,16 +421,20 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
       if (ql >= 0 && ql < P) Et[ql] = 0.0;
     }
     __syncthreads();
+    // the previous row's AB values are complete (written before this barrier)
+    if (i > 0) store_ab_row((i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp, NJ, R, Tp, tid, NT);
+    double* srow = (i & 1) ? SR1 : SR0;
     if constexpr (CHM > 0)
-      vh_row_reg<CHM>(E, NJ, w, g, warp, lane, NW, ab + (int64_t)i * T, STG + warp * 32 * CHM);
+      vh_row_reg<CHM>(E, w, g, warp, NW, srow);
     else {
-      vh_row_smem(E, SUF, PRE, NC, NJ, w, warp, lane, NW, ab + (int64_t)i * T);
+      vh_row_smem(E, SUF, PRE, NC, NJ, w, warp, lane, NW, srow);
       __syncthreads();  // SUF/PRE reused next row
     }
-    // no trailing barrier: the next row writes the other E buffer; the barrier
-    // after that row's writes orders this row's reads before row i+2's writes.
+    // no trailing barrier: the next row writes the other E / row buffer; the
+    // barrier after that row's writes orders this row's reads before row i+2's writes.
   }
   __syncthreads();
+  store_ab_row(((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp, NJ, R, Tp, tid, NT);
   E = E0;
 
   // ---- allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
@@ -487,13 +488,18 @@ __device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p
   }
   return warp_min(m);
 }
-__device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
+__device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, int lt0 = -1, int le0 = -1) {
   const int w = v.w;
   double lov = -1.0, hi = PST_INF;
   int clo = 0, chi = 2 * w;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
-    count2m(v, lane, p, lt, le);
+    if (it == 0 && lt0 >= 0) {
+      lt = lt0;
+      le = le0;
+    } else {
+      count2m(v, lane, p, lt, le);
+    }
     if (lt < k && k <= le) return p;
     const bool down = k <= lt;
     if (down) {
@@ -525,134 +531,122 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p) {
   return p;
 }
 
-// Selection kernel: one CTA per (tile, segment) of the row kernel's scratch.
-// The tile's allP_BA is staged in shared memory; each warp sweeps a
-// contiguous run of windows in chunks of JC: the chunk's AB block (w rows x JC
-// windows, coalesced row segments) is copied to a padded per-warp buffer
-// (stride JC+1, odd) so that reading one window's column is conflict free.
-__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+// Selection kernel: one CTA per (tile, segment) of the row kernel's scratch,
+// NWS warps.  Lane L of a warp owns the run of consecutive windows
+// j = L*R + r, r in [r0, r1) (the warp's share of the run length R); the AB
+// scratch is stored in lane-run order, so at step r the warp's 32 lanes read
+// one contiguous 256-byte line per row, and lane L's column-minima window
+// BA[j .. j+w) in shared memory has lane stride R (odd: conflict free).
+//
+// Step r: every lane counts #(< p) and #(<= p) of its own 2w values with the
+// previous window's answer p as pivot (one coalesced pass, ~5 instructions
+// per element).  Where p is still the k-th smallest (53-75% of windows,
+// depending on m) the window is done; the other lanes' windows are solved
+// one after another by the whole warp (warp_select: the column is gathered
+// into registers, lane l holding elements l, l+32, ...; the known counts seed
+// the bracketing search).  Each lane's first window is solved the same way.
+__device__ __forceinline__ double e_to_dist(double ev, double twol) {
+  if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
+  if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
+  return sqrt(twol * ev);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
+// exact k-th smallest of window (lane L, step r), whole warp; TM = 0: long
+// windows, values re-read from memory on every pass.  fresh: no pivot yet
+// (answers may be tiny negative residues, so no sentinel value is used).
 template <int TM>
-__global__ void __launch_bounds__(256, 1) k_select(const MPArgs a, int NCmax, int JC) {
-  extern __shared__ double smb[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int w = (int)a.w, T = (int)a.T;
-  const int64_t J0 = (int64_t)blockIdx.x * a.T;
-  const int NJ = (int)min(a.T, a.N - J0);
-  const int NC = NJ + w - 1;
-  const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  const double* ab = a.ab + cta * ((int64_t)w * T);
-  const double* bag = a.ba + cta * NCmax;
-  double* BA = smb;
-  const int SJ = JC + 1;
-  double* cbuf[2];
-  cbuf[0] = smb + NCmax + warp * (2 * w * SJ);
-  cbuf[1] = cbuf[0] + w * SJ;
-  const int per = (NJ + 7) / 8;
-  const int j0 = min(NJ, warp * per), j1 = min(NJ, j0 + per);
-  const int rpi = 32 / JC;  // rows per copy instruction (JC <= 32, power of two)
-  const int cj = lane % JC, r0 = lane / JC;
-  auto stage = [&](int jc, double* dst) {  // AB[0..w)[jc .. jc+JC) -> dst[i*SJ + jj]
-    const int nj = min(JC, j1 - jc);
-    if (cj < nj)
-      for (int i = r0; i < w; i += rpi) cp_async8(dst + i * SJ + cj, ab + (int64_t)i * T + jc + cj);
-    cp_async_commit();
-  };
-  if (j0 < j1) stage(j0, cbuf[0]);
-  for (int c = tid; c < NC; c += 256) BA[c] = bag[c];
-  __syncthreads();
-  const double twol = 2.0 * (double)a.l;
-  double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
-  double p = -1.0;
-  int cur = 0;
-  for (int jc = j0; jc < j1; jc += JC, cur ^= 1) {
-    const int nj = min(JC, j1 - jc);
-    if (jc + JC < j1) {
-      stage(jc + JC, cbuf[cur ^ 1]);  // prefetch the next chunk
-      cp_async_wait1();
-    } else {
-      cp_async_wait0();
-    }
-    __syncwarp();
-    const double* chunk = cbuf[cur];
-    double outv = 0.0;
-    for (int jj = 0; jj < nj; ++jj) {
-      const int j = jc + jj;
-      const double* Bw = BA + j;
-      WinVals<TM> v;
-      const double* ca = chunk + lane * SJ + jj;
-      const double* cb = Bw + lane;
+__device__ __forceinline__ double solve_window(const double* __restrict__ ab, const double* BA, int w, int k,
+                                               int R, int Tp, int L, int r, int lane, bool fresh, double piv,
+                                               int lt0, int le0) {
+  const double* Ac = ab + r * 32 + L;
+  const double* Bc = BA + L * R + r;
+  if constexpr (TM > 0) {
+    WinVals<TM> v;
 #pragma unroll
-      for (int t = 0; t < TM; ++t) {
-        const bool ok = lane + 32 * t < w;
-        v.a[t] = ok ? ca[32 * t * SJ] : PST_INF;
-        v.b[t] = ok ? cb[32 * t] : PST_INF;
-      }
-      double ans;
-      if (2 * w <= (int)a.k) {
-        double m = -PST_INF;
-#pragma unroll
-        for (int t = 0; t < TM; ++t)
-          if (lane + 32 * t < w) m = dmax(m, dmax(v.a[t], v.b[t]));
-        ans = warp_max(m);
-      } else {
-        if (p < 0.0) p = dmax(warp_max(v.a[0] < PST_INF ? v.a[0] : -PST_INF) * 0.25, 0.0);
-        ans = warp_select<TM>(v, w, (int)a.k, p);
-      }
-      p = ans;
-      if (lane == jj) outv = ans;
+    for (int t = 0; t < TM; ++t) {
+      const int i = lane + 32 * t;
+      const bool ok = i < w;
+      v.a[t] = ok ? __ldg(Ac + (int64_t)i * Tp) : PST_INF;
+      v.b[t] = ok ? Bc[i] : PST_INF;
     }
-    if (lane < nj) {
-      double ev = outv;
-      if (ev < 1e-15) ev = 0.0;  // rounding noise of an exact match (rho == 1)
-      if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
-      Drow[jc + lane] = sqrt(twol * ev);
-    }
-    __syncwarp();  // chunk buffer is overwritten by the prefetch two chunks later
+    if (fresh) piv = dmax(warp_max(v.a[0] < PST_INF ? v.a[0] : -PST_INF) * 0.25, 0.0);
+    return warp_select<TM>(v, w, k, piv, lt0, le0);
+  } else {
+    MemWin v{Ac, Bc, w, (int64_t)Tp};
+    if (fresh) piv = dmax(warp_max(lane < w ? __ldg(Ac + (int64_t)lane * Tp) : -PST_INF) * 0.25, 0.0);
+    return warp_select_mem(v, lane, k, piv, lt0, le0);
   }
 }
 
-// Selection for very long windows (2w > 1024 elements): column gathered straight
-// from the row-major AB scratch (stride T), passes re-read memory.
-__global__ void __launch_bounds__(256) k_select_big(const MPArgs a, int NCmax) {
+template <int NWS, int TM>
+__global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int NCmax) {
   extern __shared__ double smb[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int w = (int)a.w, T = (int)a.T;
+  const int w = (int)a.w, R = (int)a.R, Tp = (int)a.Tp, k = (int)a.k;
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  const double* ab = a.ab + cta * ((int64_t)w * T);
-  const double* bag = a.ba + cta * NCmax;
-  for (int c = tid; c < NC; c += 256) smb[c] = bag[c];
+  const double* __restrict__ ab = a.ab + cta * ((int64_t)w * Tp);
+  const double* __restrict__ bag = a.ba + cta * NCmax;
+  double* BA = smb;
+  for (int c = tid; c < NC; c += NWS * 32) BA[c] = bag[c];
   __syncthreads();
   const double twol = 2.0 * (double)a.l;
   double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
-  const int per = (NJ + 7) / 8;
-  const int j0 = min(NJ, warp * per), j1 = min(NJ, j0 + per);
-  double p = -1.0;
-  for (int j = j0; j < j1; ++j) {
-    MemWin v{ab + j, smb + j, w, (int64_t)T};
-    double ans;
-    if (2 * w <= (int)a.k) {
-      double m = -PST_INF;
-      for (int i = lane; i < w; i += 32) m = dmax(m, dmax(v.A[i * v.sa], v.B[i]));
-      ans = warp_max(m);
-    } else {
-      if (p < 0.0) p = dmax(warp_max(lane < w ? v.A[lane * v.sa] : -PST_INF) * 0.25, 0.0);
-      ans = warp_select_mem(v, lane, (int)a.k, p);
+  const int rper = (R + NWS - 1) / NWS;
+  const int r0 = warp * rper, r1 = min(R, r0 + rper);
+  if (r0 >= r1) return;
+  const int jl = lane * R;  // first window of this lane's run
+
+  if (2 * w <= k) {  // the k-th smallest is the maximum (mpdist.py:229-230)
+    for (int r = r0; r < r1; ++r) {
+      const int j = jl + r;
+      const bool ok = j < NJ;
+      const double* Ap = ab + r * 32 + lane;
+      const double* Bp = BA + (ok ? j : 0);
+      double mx = -PST_INF;
+#pragma unroll 8
+      for (int i = 0; i < w; ++i) mx = dmax(mx, dmax(__ldg(Ap + (int64_t)i * Tp), Bp[i]));
+      if (ok) Drow[j] = e_to_dist(mx, twol);
     }
-    p = ans;
-    double ev = ans;
-    if (ev < 1e-15) ev = 0.0;
-    if (ev > 2.0) ev = 2.0;
-    if (lane == 0) Drow[j] = sqrt(twol * ev);
+    return;
+  }
+
+  // first window of every lane's run, lanes in turn; lane L starts from lane
+  // L-1's answer (its window lies R to the left)
+  double p = 0.0;
+  {
+    double prev = 0.0;
+    for (int L = 0; L < 32; ++L) {
+      if (L * R + r0 >= NJ) break;  // warp-uniform
+      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1);
+      if (lane == L) p = prev;
+    }
+    if (jl + r0 < NJ) Drow[jl + r0] = e_to_dist(p, twol);
+  }
+  for (int r = r0 + 1; r < r1; ++r) {
+    const int j = jl + r;
+    const bool ok = j < NJ;
+    const double* Ap = ab + r * 32 + lane;
+    const double* Bp = BA + (ok ? j : 0);
+    int lt = 0, le = 0;
+#pragma unroll 8
+    for (int i = 0; i < w; ++i) {
+      const double va = __ldg(Ap + (int64_t)i * Tp), vb = Bp[i];
+      lt += (va < p) + (vb < p);
+      le += (va <= p) + (vb <= p);
+    }
+    unsigned pend = __ballot_sync(FULLMASK, ok && !(lt < k && k <= le));
+    while (pend) {
+      const int L = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const double pl = __shfl_sync(FULLMASK, p, L);
+      const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
+      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel);
+      if (lane == L) p = x;
+    }
+    if (ok) Drow[j] = e_to_dist(p, twol);
   }
 }
 
@@ -670,16 +664,10 @@ int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
   return PST_OK;
 }
 
-// P (columns per thread) is odd so the per-thread E[] stores are bank-conflict free.
-template <int TM>
-int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0) {
-  auto kern = k_select<TM>;
-  // per-warp chunk of JC windows (power of two <= 32), padded stride JC+1
-  // chunk width: small enough for >= 4 CTAs (32 warps) per SM -- the per-window
-  // work is a latency chain, so occupancy matters more than chunk length
-  int JC = 32;
-  while (JC > 4 && (size_t)16 * a.w * (JC + 1) * sizeof(double) + smem0 > 52 * 1024) JC /= 2;
-  const size_t smem = smem0 + (size_t)16 * a.w * (JC + 1) * sizeof(double);
+template <int NWS, int TM>
+int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
+  const size_t smem = (size_t)NCmax * sizeof(double);
+  auto kern = k_select_run<NWS, TM>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -687,39 +675,34 @@ int launch_sel_t(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax, size_t smem0
       return PST_ECUDA;
     }
   }
-  kern<<<grid, 256, smem, c->st2>>>(a, NCmax, JC);
+  kern<<<grid, NWS * 32, smem, c->st2>>>(a, NCmax);
   c->launches++;
   PST_CUDA(cudaGetLastError());
   return PST_OK;
 }
 
-int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int tm, int NCmax, size_t smem) {
-  switch (tm) {
-    case 1: return launch_sel_t<1>(c, a, grid, NCmax, smem);
-    case 2: return launch_sel_t<2>(c, a, grid, NCmax, smem);
-    case 3: return launch_sel_t<3>(c, a, grid, NCmax, smem);
-    case 4: return launch_sel_t<4>(c, a, grid, NCmax, smem);
-    case 5: return launch_sel_t<5>(c, a, grid, NCmax, smem);
-    case 6: return launch_sel_t<6>(c, a, grid, NCmax, smem);
-    case 7: return launch_sel_t<7>(c, a, grid, NCmax, smem);
-    case 8: return launch_sel_t<8>(c, a, grid, NCmax, smem);
-    case 9: return launch_sel_t<9>(c, a, grid, NCmax, smem);
-    default: break;
-  }
-  if (tm <= 12) return launch_sel_t<12>(c, a, grid, NCmax, smem);
-  if (tm <= 16) return launch_sel_t<16>(c, a, grid, NCmax, smem);
-  {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k_select_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) {
-        pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
-        return PST_ECUDA;
-      }
-    }
-    k_select_big<<<grid, 256, smem, c->st2>>>(a, NCmax);
-    c->launches++;
-    PST_CUDA(cudaGetLastError());
-    return PST_OK;
+// warps per selection CTA: each warp's share of the run stays >= ~12 windows
+// so the warp-cooperative run starts are amortized.
+template <int TM>
+int launch_sel_tm(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
+  if (a.R >= 48) return launch_sel_w<4, TM>(c, a, grid, NCmax);
+  if (a.R >= 24) return launch_sel_w<2, TM>(c, a, grid, NCmax);
+  return launch_sel_w<1, TM>(c, a, grid, NCmax);
+}
+
+// TM = ceil(w / 32) values of each half per lane in the warp-cooperative path
+int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
+  switch ((int)((a.w + 31) >> 5)) {
+    case 1: return launch_sel_tm<1>(c, a, grid, NCmax);
+    case 2: return launch_sel_tm<2>(c, a, grid, NCmax);
+    case 3: return launch_sel_tm<3>(c, a, grid, NCmax);
+    case 4: return launch_sel_tm<4>(c, a, grid, NCmax);
+    case 5: return launch_sel_tm<5>(c, a, grid, NCmax);
+    case 6: return launch_sel_tm<6>(c, a, grid, NCmax);
+    case 7: return launch_sel_tm<7>(c, a, grid, NCmax);
+    case 8: return launch_sel_tm<8>(c, a, grid, NCmax);
+    case 9: return launch_sel_tm<9>(c, a, grid, NCmax);
+    default: return launch_sel_tm<0>(c, a, grid, NCmax);
   }
 }
 
@@ -771,7 +754,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
     const int64_t ncm = (int64_t)tt * pp;
-    return (size_t)(l + 4 * w + ncm * (chm ? 2 : 4) + 64 + 2 + (tt / 32) * 32 * (chm ? chm : 1)) * sizeof(double);
+    return (size_t)(l + 4 * w + ncm * (chm ? 4 : 6) + 64 + 2) * sizeof(double);
   };
   while (P > 1 && smem_for(P, nt) > smax) P -= 2;
   if (smem_for(P, nt) > smax || (int64_t)nt * P < w) {
@@ -794,9 +777,11 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   if (T > N) T = N;
   if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < T) T = v; }
   const int64_t ntile = (N + T - 1) / T;
+  const int64_t R = ((T + 31) / 32) | 1;  // lane-run length (odd), AB row stride 32*R
+  const int64_t Tp = 32 * R;
   // scratch: AB (S*T doubles) + allP_BA (NCmax doubles) per CTA, two buffers so the
   // selection of batch b (stream st2) overlaps the row loop of batch b+1 (stream st).
-  const size_t ab_cta = (size_t)w * (size_t)T * sizeof(double);
+  const size_t ab_cta = (size_t)w * (size_t)Tp * sizeof(double);
   const size_t per_cta = ab_cta + (size_t)NCmax * sizeof(double);
   size_t budget = (size_t)6 << 30;
   {
@@ -822,6 +807,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
   a.df = c->L.df; a.dg = c->L.dg;
   a.n = n; a.l = l; a.m = m; a.w = w; a.k = k; a.Nl = Nl; a.N = N; a.T = T;
+  a.R = R; a.Tp = Tp;
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
   a.dbg_nostore = getenv("PASTILA_NOSTORE") ? 1 : 0;
@@ -831,8 +817,6 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
   }
   const size_t smem = smem_for(P, nt);
-  const int tm = (int)((w + 31) >> 5);
-  const size_t smem_sel = (size_t)NCmax * sizeof(double);
   // the selection stream starts after everything queued before on the main stream
   PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
   PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[1], 0));
@@ -852,7 +836,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     if (r != PST_OK) return r;
     PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
     PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));
-    r = launch_sel(c, a, grid, tm, (int)NCmax, smem_sel);
+    r = launch_sel(c, a, grid, (int)NCmax);
     if (r != PST_OK) return r;
     PST_CUDA(cudaEventRecord(c->ev_sel[bi], c->st2));
   }

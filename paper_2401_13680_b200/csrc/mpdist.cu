@@ -210,14 +210,32 @@ __device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, 
 // One AB row from the CTA row buffer to HBM in lane-run order: window
 // j = L*R + r (L = 0..31, r = 0..R-1) is stored at r*32 + L, so that the 32
 // lanes of a selection warp, which sweep windows L*R + r for r = 0, 1, ...,
-// read one contiguous 256-byte line per row.  Shared reads srow[L*R + r] have
-// odd stride R (bank-conflict free); global stores are contiguous.
-__device__ __forceinline__ void store_ab_row(const double* __restrict__ srow, double* __restrict__ dst, int NJ,
-                                             int R, int Tp, int tid, int nt) {
-  for (int pos = tid; pos < Tp; pos += nt) {
-    const int j = (pos & 31) * R + (pos >> 5);
-    if (j < NJ) dst[pos] = srow[j];
-  }
+// read one contiguous 256-byte line per row.  Thread tid always moves the
+// same positions (lane L = tid%32, r = tid/32 + c*NT/32), so the offsets are
+// set up once per tile and each element is one LDS + one STG; shared reads
+// srow[L*R + r] have odd stride R (bank-conflict free), global stores are
+// contiguous.  At most MAXC = P+1 elements per thread (T <= NT*P).
+struct AbStore {
+  int src, dst, cnt;
+};
+template <int NT>
+__device__ __forceinline__ AbStore ab_store_setup(int NJ, int R, int tid) {
+  const int L = tid & 31, r0 = tid >> 5;
+  const int j0 = L * R + r0, jend = min(NJ, (L + 1) * R);
+  AbStore s;
+  s.src = j0;
+  s.dst = r0 * 32 + L;
+  s.cnt = j0 < jend ? (jend - j0 + NT / 32 - 1) / (NT / 32) : 0;
+  return s;
+}
+template <int NT, int MAXC>
+__device__ __forceinline__ void store_ab_row(const AbStore& g, const double* __restrict__ srow,
+                                             double* __restrict__ dst) {
+  const double* s = srow + g.src;
+  double* d = dst + g.dst;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+    if (c < g.cnt) d[c * NT] = s[c * (NT / 32)];
 }
 
 // van Herk, shared-memory version for large w (chunks do not fit registers).
@@ -268,7 +286,7 @@ __device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double
 }
 
 template <int P, int NT, int CHM>
-__global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(const MPArgs a) {
+__global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(const MPArgs a) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
@@ -381,6 +399,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
     g.u0 = g.ll * (CHM > 0 ? CHM : 1);
   }
   const bool tail = (tid + 1) * P > NC;  // this thread owns columns past the tile's last one
+  const AbStore abst = ab_store_setup<NT>(NJ, R, tid);
   for (int i = 0; i < w; ++i) {
     double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
     if (i > 0) {
@@ -422,7 +441,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
     }
     __syncthreads();
     // the previous row's AB values are complete (written before this barrier)
-    if (i > 0) store_ab_row((i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp, NJ, R, Tp, tid, NT);
+    if (i > 0) store_ab_row<NT, P + 1>(abst, (i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp);
     double* srow = (i & 1) ? SR1 : SR0;
     if constexpr (CHM > 0)
       vh_row_reg<CHM>(E, w, g, warp, NW, srow);
@@ -434,7 +453,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(co
     // barrier after that row's writes orders this row's reads before row i+2's writes.
   }
   __syncthreads();
-  store_ab_row(((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp, NJ, R, Tp, tid, NT);
+  store_ab_row<NT, P + 1>(abst, ((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp);
   E = E0;
 
   // ---- allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
@@ -539,8 +558,9 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, in
 // BA[j .. j+w) in shared memory has lane stride R (odd: conflict free).
 //
 // Step r: every lane counts #(< p) and #(<= p) of its own 2w values with the
-// previous window's answer p as pivot (one coalesced pass, ~5 instructions
-// per element).  Where p is still the k-th smallest (53-75% of windows,
+// previous window's answer p as pivot: the w row minima in one coalesced pass
+// (~4 instructions per element), the w column minima incrementally (the B
+// window slides by one; recounted whenever p changes).  Where p is still the k-th smallest (53-75% of windows,
 // depending on m) the window is done; the other lanes' windows are solved
 // one after another by the whole warp (warp_select: the column is gathered
 // into registers, lane l holding elements l, l+32, ...; the known counts seed
@@ -554,12 +574,15 @@ __device__ __forceinline__ double e_to_dist(double ev, double twol) {
 // exact k-th smallest of window (lane L, step r), whole warp; TM = 0: long
 // windows, values re-read from memory on every pass.  fresh: no pivot yet
 // (answers may be tiny negative residues, so no sentinel value is used).
+// Also returns #(B < ans) and #(B <= ans) for the lane's incremental B counts.
 template <int TM>
 __device__ __forceinline__ double solve_window(const double* __restrict__ ab, const double* BA, int w, int k,
                                                int R, int Tp, int L, int r, int lane, bool fresh, double piv,
-                                               int lt0, int le0) {
+                                               int lt0, int le0, int& ltB, int& leB) {
   const double* Ac = ab + r * 32 + L;
   const double* Bc = BA + L * R + r;
+  double x;
+  int b1 = 0, b2 = 0;
   if constexpr (TM > 0) {
     WinVals<TM> v;
 #pragma unroll
@@ -570,12 +593,24 @@ __device__ __forceinline__ double solve_window(const double* __restrict__ ab, co
       v.b[t] = ok ? Bc[i] : PST_INF;
     }
     if (fresh) piv = dmax(warp_max(v.a[0] < PST_INF ? v.a[0] : -PST_INF) * 0.25, 0.0);
-    return warp_select<TM>(v, w, k, piv, lt0, le0);
+    x = warp_select<TM>(v, w, k, piv, lt0, le0);
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+      b1 += v.b[t] < x;
+      b2 += v.b[t] <= x;
+    }
   } else {
     MemWin v{Ac, Bc, w, (int64_t)Tp};
     if (fresh) piv = dmax(warp_max(lane < w ? __ldg(Ac + (int64_t)lane * Tp) : -PST_INF) * 0.25, 0.0);
-    return warp_select_mem(v, lane, k, piv, lt0, le0);
+    x = warp_select_mem(v, lane, k, piv, lt0, le0);
+    for (int i = lane; i < w; i += 32) {
+      b1 += Bc[i] < x;
+      b2 += Bc[i] <= x;
+    }
   }
+  ltB = __reduce_add_sync(FULLMASK, b1);
+  leB = __reduce_add_sync(FULLMASK, b2);
+  return x;
 }
 
 template <int NWS, int TM>
@@ -614,14 +649,21 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
   }
 
   // first window of every lane's run, lanes in turn; lane L starts from lane
-  // L-1's answer (its window lies R to the left)
+  // L-1's answer (its window lies R to the left).  ltB/leB: this lane's counts
+  // of its B window (BA[j .. j+w)) below / at-or-below p, kept incrementally.
   double p = 0.0;
+  int ltB = 0, leB = 0;
   {
     double prev = 0.0;
     for (int L = 0; L < 32; ++L) {
       if (L * R + r0 >= NJ) break;  // warp-uniform
-      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1);
-      if (lane == L) p = prev;
+      int b1, b2;
+      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2);
+      if (lane == L) {
+        p = prev;
+        ltB = b1;
+        leB = b2;
+      }
     }
     if (jl + r0 < NJ) Drow[jl + r0] = e_to_dist(p, twol);
   }
@@ -629,13 +671,17 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
     const int j = jl + r;
     const bool ok = j < NJ;
     const double* Ap = ab + r * 32 + lane;
-    const double* Bp = BA + (ok ? j : 0);
-    int lt = 0, le = 0;
+    if (ok) {  // slide the B window: BA[j-1] leaves, BA[j+w-1] enters
+      const double out = BA[j - 1], in = BA[j + w - 1];
+      ltB += (in < p) - (out < p);
+      leB += (in <= p) - (out <= p);
+    }
+    int lt = ltB, le = leB;
 #pragma unroll 8
     for (int i = 0; i < w; ++i) {
-      const double va = __ldg(Ap + (int64_t)i * Tp), vb = Bp[i];
-      lt += (va < p) + (vb < p);
-      le += (va <= p) + (vb <= p);
+      const double va = __ldg(Ap + (int64_t)i * Tp);
+      lt += va < p;
+      le += va <= p;
     }
     unsigned pend = __ballot_sync(FULLMASK, ok && !(lt < k && k <= le));
     while (pend) {
@@ -643,8 +689,13 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
       pend &= pend - 1;
       const double pl = __shfl_sync(FULLMASK, p, L);
       const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
-      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel);
-      if (lane == L) p = x;
+      int b1, b2;
+      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1, b2);
+      if (lane == L) {
+        p = x;
+        ltB = b1;
+        leB = b2;
+      }
     }
     if (ok) Drow[j] = e_to_dist(p, twol);
   }
@@ -708,9 +759,9 @@ int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
 
 template <int NT>
 int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, int chm, size_t smem) {
-  if (chm == 3) return P == 5 ? launch_p<5, NT, 3>(c, a, grid, smem) : launch_p<7, NT, 3>(c, a, grid, smem);
-  if (chm == 5) return P == 5 ? launch_p<5, NT, 5>(c, a, grid, smem) : launch_p<7, NT, 5>(c, a, grid, smem);
-  if (chm == 9) return P == 5 ? launch_p<5, NT, 9>(c, a, grid, smem) : launch_p<7, NT, 9>(c, a, grid, smem);
+  if (chm == 3) return P == 5 ? launch_p<5, NT, 3>(c, a, grid, smem) : launch_p<3, NT, 3>(c, a, grid, smem);
+  if (chm == 5) return P == 5 ? launch_p<5, NT, 5>(c, a, grid, smem) : launch_p<3, NT, 5>(c, a, grid, smem);
+  if (chm == 9) return P == 5 ? launch_p<5, NT, 9>(c, a, grid, smem) : launch_p<3, NT, 9>(c, a, grid, smem);
   switch (P) {
     case 9: return launch_p<9, NT, 0>(c, a, grid, smem);
     case 7: return launch_p<7, NT, 0>(c, a, grid, smem);
@@ -748,14 +799,21 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
   // tile geometry: NC = NT*P columns, T = NC - w + 1 windows; aim for T >= 4w
   int nt = (4 * w > 256 * 5) ? 512 : 256;
+  if (const char* e = getenv("PASTILA_NT_W")) nt = (w >= atoll(e)) ? 512 : 256;  // tuning experiments
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class
-  const int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 288) ? 9 : 0;
+  // columns per lane in the register van Herk (measured best on B200, tools/tune.py)
+  int chm = (w <= 24) ? 3 : (w <= 128) ? 9 : (w <= 160) ? 5 : (w <= 288) ? 9 : 0;
+  if (const char* e = getenv("PASTILA_CHM")) {  // tuning experiments
+    const int v = atoi(e);
+    if ((v == 3 || v == 5 || v == 9) && 32 * v >= w) chm = v;
+  }
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
     const int64_t ncm = (int64_t)tt * pp;
     return (size_t)(l + 4 * w + ncm * (chm ? 4 : 6) + 64 + 2) * sizeof(double);
   };
+  if (const char* e = getenv("PASTILA_P")) { const int v = atoi(e); if (v == 3 || v == 5) P = v; }  // tuning
   while (P > 1 && smem_for(P, nt) > smax) P -= 2;
   if (smem_for(P, nt) > smax || (int64_t)nt * P < w) {
     pst_set_error("snippet size %lld too large for shared-memory tiles", (long long)m);

@@ -14,7 +14,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libpastila.so"
+# PASTILA_LIB: alternative in-tree build (kernel tuning experiments)
+LIB_PATH = Path(os.environ.get("PASTILA_LIB") or (Path(__file__).resolve().parent / "libpastila.so"))
 
 PST_OK, PST_EINVAL, PST_ECUDA, PST_ENOMEM, PST_ESTATE = 0, -1, -2, -3, -4
 

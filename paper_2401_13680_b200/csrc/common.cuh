@@ -98,6 +98,8 @@ struct MPArgs {
   double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
   double* ba;        // scratch: allP_BA per CTA (NCmax doubles)
   int dbg_nostore;   // debug: skip AB stores (timing experiments only)
+  int dbg_flags;     // debug (PASTILA_DBGF, timing experiments only, wrong results):
+                     //   1 = selection: skip unsettled-window solves, 2 = selection: skip count pass
 };
 
 int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,

@@ -207,6 +207,62 @@ __device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, 
   }
 }
 
+// Two rows per barrier: 2*nblk (row, block) tasks over the lane groups, so
+// that long windows (few blocks per tile) keep more warps busy.
+template <int CH>
+__device__ __forceinline__ void vh_rows2_reg(const double* __restrict__ E0, const double* __restrict__ E1,
+                                             int ntask, int w, const VHGeom& g, int warp, int nw,
+                                             double* __restrict__ S0, double* __restrict__ S1) {
+  for (int t0 = warp * g.bpw; t0 < ntask; t0 += nw * g.bpw) {  // warp-uniform trip count
+    const int tau = t0 + g.sub;
+    const bool live = tau < ntask;
+    const bool second = tau >= g.nblk;
+    const double* E = second ? E1 : E0;
+    const int bb = (second ? tau - g.nblk : tau) * w, bn = bb + w;
+    double sf[CH], pr[CH];
+    double run = PST_INF;
+#pragma unroll
+    for (int t = CH - 1; t >= 0; --t) {
+      const int u = g.u0 + t;
+      const double v = (live && u < w) ? E[bb + u] : PST_INF;
+      run = dmin(run, v);
+      sf[t] = run;
+    }
+    double totS = run;
+    run = PST_INF;
+#pragma unroll
+    for (int t = 0; t < CH; ++t) {
+      const int u = g.u0 + t;
+      const double v = (live && u < w) ? E[bn + u] : PST_INF;
+      run = dmin(run, v);
+      pr[t] = run;
+    }
+    double totP = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      if (off < g.LPB) {
+        const double ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
+        const double dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
+        totS = dmin(totS, ds);
+        totP = dmin(totP, dp);
+      }
+    }
+    double cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
+    double cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
+    if (g.ll == g.LPB - 1) cs = PST_INF;
+    if (g.ll == 0) cp = PST_INF;
+    const double C = dmin(cs, cp);
+    if (live) {
+      double* st = (second ? S1 : S0) + bb;
+#pragma unroll
+      for (int t = 0; t < CH; ++t) {
+        const int u = g.u0 + t;
+        if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
+      }
+    }
+  }
+}
+
 // One AB row from the CTA row buffer to HBM in lane-run order: window
 // j = L*R + r (L = 0..31, r = 0..R-1) is stored at r*32 + L, so that the 32
 // lanes of a selection warp, which sweep windows L*R + r for r = 0, 1, ...,
@@ -472,6 +528,232 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   }
 }
 
+// Row loop, two query rows per barrier (register van Herk only).  Each thread
+// also carries one ghost column (its left neighbour's last column), so the
+// second row of a pair needs no cross-warp exchange: at the start of a pair
+// the neighbour's last two covariances arrive by shuffle (or, for lane 0, via
+// shared memory from the previous warp), the ghost is advanced with the first
+// row, and the second row uses it.  Same arithmetic as k_mpdist (bit-identical
+// e values); half the barriers and twice the van Herk tasks per phase.
+template <int P, int NT, int CHM>
+__global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(const MPArgs a) {
+  static_assert(CHM > 0, "two-row kernel uses the register van Herk");
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = NT / 32;
+  constexpr int NCmax = NT * P;
+  const int l = (int)a.l, w = (int)a.w;
+  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t J0 = (int64_t)blockIdx.x * a.T;
+  const int NJ = (int)min(a.T, a.N - J0);
+  const int NC = NJ + w - 1;
+  double* xs = sm;               // [l]
+  double* edge = xs + l;         // [w]
+  double* rdf = edge + w;        // [w] df[q-1] per row
+  double* rdg = rdf + w;         // [w] dg[q-1] per row
+  double* rnq = rdg + w;         // [w] nrm[q] per row
+  double* EB = rnq + w;          // [4][NCmax] e rows: (pair parity, row of pair); later allP_BA
+  double* SRB = EB + 4 * NCmax;  // [4][NCmax] AB row buffers
+  double* xfer = SRB + 4 * NCmax;  // [2 parity][2][32] last two covariances of each warp
+  double* red = xfer + 128;      // [2]
+  const int R = (int)a.R, Tp = (int)a.Tp;
+  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
+  const double* __restrict__ xJ = a.x + J0;
+  const double* __restrict__ xQ = a.x + q0;
+  const double* __restrict__ muJ = a.mu + J0;
+  const double* __restrict__ muQ = a.mu + q0;
+
+  // ---- row-0 fresh dots (as k_mpdist)
+  {
+    const double mq = muQ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xQ[t] - mq;
+    __syncthreads();
+    if (tid == 0) {
+      double s1 = 0.0;
+      for (int t = 0; t < l; ++t) s1 += xs[t];
+      red[0] = s1;
+    }
+    __syncthreads();
+  }
+  double cov[P];
+  {
+    const double sx = red[0];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int cl = tid * P + p;
+      double acc = 0.0;
+      if (cl < NC) {
+        const double* xc = xJ + cl;
+        for (int t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
+        acc = fma(-muJ[cl], sx, acc);
+      }
+      cov[p] = acc;
+    }
+  }
+  __syncthreads();
+  {  // left edge (column J0) for rows 1..w-1
+    const double mc = muJ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xJ[t] - mc;
+    __syncthreads();
+    if (tid == 0) {
+      double s1 = 0.0;
+      for (int t = 0; t < l; ++t) s1 += xs[t];
+      red[1] = s1;
+    }
+    __syncthreads();
+    const double sx = red[1];
+    for (int i = 1 + tid; i < w; i += NT) {
+      const double* xq = xQ + i;
+      double acc = 0.0;
+      for (int t = 0; t < l; ++t) acc = fma(xq[t], xs[t], acc);
+      edge[i] = fma(-muQ[i], sx, acc);
+    }
+  }
+  for (int i = tid; i < w; i += NT) {
+    rdf[i] = i > 0 ? a.df[q0 + i - 1] : 0.0;
+    rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
+    rnq[i] = a.nrm[q0 + i];
+  }
+  double dgc[P], dfc[P], nrmc[P], bic[P], colmin[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int cl = tid * P + p;
+    const bool ok = cl < NC;
+    const int64_t c = J0 + cl;
+    dgc[p] = (ok && c > 0) ? a.dg[c - 1] : 0.0;
+    dfc[p] = (ok && c > 0) ? a.df[c - 1] : 0.0;
+    nrmc[p] = ok ? a.nrm[c] : 0.0;
+    bic[p] = ok ? a.bias[c] : PST_INF;
+    colmin[p] = PST_INF;
+  }
+  // ghost column c0-1 (c0 = J0 + tid*P): its recurrence constants
+  double dgG = 0.0, dfG = 0.0;
+  if (tid > 0) {
+    const int64_t cg = J0 + tid * P - 1;
+    if (cg > 0 && tid * P - 1 < NC) {
+      dgG = a.dg[cg - 1];
+      dfG = a.df[cg - 1];
+    }
+  }
+  if (lane == 31) {  // row-0 covariances for the next warp's lane 0
+    xfer[0 * 64 + 0 * 32 + warp] = cov[P - 2 >= 0 ? P - 2 : 0];
+    xfer[0 * 64 + 1 * 32 + warp] = cov[P - 1];
+  }
+  __syncthreads();
+
+  const int qloc = (int)(q0 - J0) - tid * P;
+  VHGeom g;
+  {
+    int LPB = 1;
+    while (LPB < 32 && LPB * CHM < w) LPB *= 2;
+    if (LPB < 8) LPB = 8;
+    g.LPB = LPB;
+    g.bpw = 32 / LPB;
+    g.sub = lane / LPB;
+    g.ll = lane % LPB;
+    g.nblk = (NJ + w - 1) / w;
+    g.u0 = g.ll * CHM;
+  }
+  const bool tail = (tid + 1) * P > NC;
+  const AbStore abst = ab_store_setup<NT>(NJ, R, tid);
+
+  // e-values of one row from its covariances -> shared row, column minima
+  auto emit_row = [&](const double* cv, int i, double* Et) {
+    const double nq = rnq[i];
+    if (nq != 0.0) {
+      const double mnq = -nq;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const double e = fma(cv[p] * mnq, nrmc[p], bic[p]);
+        colmin[p] = dmin(colmin[p], e);
+        Et[p] = e;
+      }
+      if (tail) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          if (tid * P + p >= NC) Et[p] = PST_INF;
+      }
+    } else {  // constant query window (row-uniform branch): zdist.py:111-112
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int cl = tid * P + p;
+        const double e = (cl < NC) ? a.cbias[J0 + cl] : PST_INF;
+        colmin[p] = dmin(colmin[p], e);
+        Et[p] = e;
+      }
+    }
+    const int ql = qloc + i;  // self column (zdist.py:121-122)
+    if (ql >= 0 && ql < P) Et[ql] = 0.0;
+  };
+
+  const int npair = (w + 1) / 2;
+  for (int it = 0; it < npair; ++it) {
+    const int i0 = 2 * it, i1 = i0 + 1;
+    const bool has1 = i1 < w;
+    const int par = it & 1;
+    // neighbour's last two covariances of the current state (row i0-1, or row 0 when it == 0)
+    double g1 = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
+    double g2 = __shfl_up_sync(FULLMASK, cov[P >= 2 ? P - 2 : 0], 1);
+    if (lane == 0 && warp > 0) {
+      g2 = xfer[par * 64 + 0 * 32 + warp - 1];
+      g1 = xfer[par * 64 + 1 * 32 + warp - 1];
+    }
+    double r0v[P];
+    double gh;  // ghost column (c0-1) at row i0
+    if (it == 0) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) r0v[p] = cov[p];
+      gh = g1;
+    } else {
+      const double dfq = rdf[i0], dgq = rdg[i0];
+#pragma unroll
+      for (int p = P - 1; p >= 1; --p) r0v[p] = fma(dfq, dgc[p], fma(dgq, dfc[p], cov[p - 1]));
+      r0v[0] = (tid == 0) ? edge[i0] : fma(dfq, dgc[0], fma(dgq, dfc[0], g1));
+      gh = fma(dfq, dgG, fma(dgq, dfG, g2));
+    }
+    emit_row(r0v, i0, EB + (par * 2 + 0) * NCmax + tid * P);
+    if (has1) {
+      const double dfq = rdf[i1], dgq = rdg[i1];
+#pragma unroll
+      for (int p = P - 1; p >= 1; --p) cov[p] = fma(dfq, dgc[p], fma(dgq, dfc[p], r0v[p - 1]));
+      cov[0] = (tid == 0) ? edge[i1] : fma(dfq, dgc[0], fma(dgq, dfc[0], gh));
+      emit_row(cov, i1, EB + (par * 2 + 1) * NCmax + tid * P);
+      if (lane == 31) {
+        xfer[(par ^ 1) * 64 + 0 * 32 + warp] = cov[P >= 2 ? P - 2 : 0];
+        xfer[(par ^ 1) * 64 + 1 * 32 + warp] = cov[P - 1];
+      }
+    }
+    __syncthreads();
+    if (it > 0) {  // AB rows of the previous pair are complete
+      const int pp = par ^ 1;
+      store_ab_row<NT, P + 1>(abst, SRB + (pp * 2 + 0) * NCmax, ab + (int64_t)(i0 - 2) * Tp);
+      store_ab_row<NT, P + 1>(abst, SRB + (pp * 2 + 1) * NCmax, ab + (int64_t)(i0 - 1) * Tp);
+    }
+    vh_rows2_reg<CHM>(EB + (par * 2 + 0) * NCmax, EB + (par * 2 + 1) * NCmax, g.nblk * (has1 ? 2 : 1), w, g,
+                      warp, NW, SRB + (par * 2 + 0) * NCmax, SRB + (par * 2 + 1) * NCmax);
+  }
+  __syncthreads();
+  {
+    const int it = npair - 1, par = it & 1, i0 = 2 * it;
+    store_ab_row<NT, P + 1>(abst, SRB + (par * 2 + 0) * NCmax, ab + (int64_t)i0 * Tp);
+    if (i0 + 1 < w) store_ab_row<NT, P + 1>(abst, SRB + (par * 2 + 1) * NCmax, ab + (int64_t)(i0 + 1) * Tp);
+  }
+  double* E = EB;  // allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int cl = tid * P + p;
+    const int64_t c = J0 + cl;
+    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : colmin[p];
+  }
+  __syncthreads();
+  {
+    double* bag = a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
+    for (int c = tid; c < NC; c += NT) bag[c] = E[c];
+    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+      for (int c = tid; c < NC; c += NT) a.dbg_ba[c] = E[c];
+  }
+}
+
 // Generic (memory-resident) variant of the warp selection for 2w > 32*2*16.
 struct MemWin {
   const double* A;  // row minima, stride sa
@@ -677,13 +959,18 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
       leB += (in <= p) - (out <= p);
     }
     int lt = ltB, le = leB;
-#pragma unroll 8
-    for (int i = 0; i < w; ++i) {
-      const double va = __ldg(Ap + (int64_t)i * Tp);
-      lt += va < p;
-      le += va <= p;
+    if (!(a.dbg_flags & 2)) {
+      // loads in flight per lane: the pass is a chain of HBM round trips (measured best)
+      constexpr int kSelUnroll = TM >= 7 || TM == 0 ? 32 : TM >= 4 ? 16 : 8;
+#pragma unroll kSelUnroll
+      for (int i = 0; i < w; ++i) {
+        const double va = __ldg(Ap + (int64_t)i * Tp);
+        lt += va < p;
+        le += va <= p;
+      }
     }
     unsigned pend = __ballot_sync(FULLMASK, ok && !(lt < k && k <= le));
+    if (a.dbg_flags & 1) pend = 0;
     while (pend) {
       const int L = __ffs(pend) - 1;
       pend &= pend - 1;
@@ -755,6 +1042,27 @@ int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
     case 9: return launch_sel_tm<9>(c, a, grid, NCmax);
     default: return launch_sel_tm<0>(c, a, grid, NCmax);
   }
+}
+
+template <int P, int NT, int CHM>
+int launch_p2(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
+  auto kern = k_mpdist2<P, NT, CHM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PST_ECUDA;
+  }
+  kern<<<grid, NT, smem, c->st>>>(a);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+template <int NT>
+int launch_nt2(pst_ctx* c, const MPArgs& a, dim3 grid, int chm, size_t smem) {
+  if (chm == 3) return launch_p2<5, NT, 3>(c, a, grid, smem);
+  if (chm == 5) return launch_p2<5, NT, 5>(c, a, grid, smem);
+  return launch_p2<5, NT, 9>(c, a, grid, smem);
 }
 
 template <int NT>
@@ -869,12 +1177,26 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
   a.dbg_nostore = getenv("PASTILA_NOSTORE") ? 1 : 0;
+  a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
   if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));
     a.dbg_ba = c->dbg;
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
   }
   const size_t smem = smem_for(P, nt);
+  // two rows per barrier (k_mpdist2): register van Herk, P = 5
+  const size_t smem2 = (size_t)(l + 4 * w + 8 * NCmax + 130) * sizeof(double);
+  // used when one row leaves lane-group slots idle and two rows fit one round
+  bool rows2 = false;
+  if (chm > 0 && P == 5 && smem2 <= smax) {
+    int lpb = 1;
+    while (lpb < 32 && lpb * chm < w) lpb *= 2;
+    if (lpb < 8) lpb = 8;
+    const int64_t slots = (int64_t)(nt / 32) * (32 / lpb);
+    const int64_t nblk = (std::min(T, N) + w - 1) / w;
+    rows2 = 2 * nblk <= slots;
+    if (const char* e = getenv("PASTILA_ROWS2")) rows2 = atoi(e) > 0;  // tuning experiments
+  }
   // the selection stream starts after everything queued before on the main stream
   PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
   PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[1], 0));
@@ -890,7 +1212,11 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     a.ba = (double*)(buf + ab_cta * (size_t)ntile * (size_t)segs_per);
     dim3 grid((unsigned)ntile, (unsigned)ns);
     PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[bi], 0));  // buffer bi free again
-    int r = (nt == 512) ? launch_nt<512>(c, a, grid, P, chm, smem) : launch_nt<256>(c, a, grid, P, chm, smem);
+    int r;
+    if (rows2)
+      r = (nt == 512) ? launch_nt2<512>(c, a, grid, chm, smem2) : launch_nt2<256>(c, a, grid, chm, smem2);
+    else
+      r = (nt == 512) ? launch_nt<512>(c, a, grid, P, chm, smem) : launch_nt<256>(c, a, grid, P, chm, smem);
     if (r != PST_OK) return r;
     PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
     PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));

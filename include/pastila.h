@@ -110,6 +110,16 @@ int pst_areas_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, in
  * row indices offset by row_base.  minval_dev [N], argmin_dev [N].        */
 int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
                    int64_t row_base, double* minval_dev, int32_t* argmin_dev);
+/* Profiles of segments [seg_lo, seg_hi) computed in device-sized chunks and
+ * reduced without being stored (S x N larger than HBM, C4: n = 1e7):
+ * areas_dev[s-seg_lo] = sum_j min(D[s][j], curve_dev[j]) (curve NULL: +inf);
+ * if minval_dev/argmin_dev are given, running per-window minimum and first
+ * argmin (segment index, caller initialises minval to +inf); if rowmax_dev
+ * is given, running max (caller initialises it to 0.0).  Serves the greedy
+ * rounds of select_snippets (snippets.py:201-213) and segment-row sharding. */
+int pst_profile_reduce_dev(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                           const double* curve_dev, double* areas_dev, double* minval_dev,
+                           int32_t* argmin_dev, double* rowmax_dev);
 /* The context's CUDA stream (cudaStream_t) for caller-side event timing.  */
 int pst_stream(pst_ctx* ctx, void** stream_out);
 /* Profile-kernel timing: pst_timing(ctx,1) enables + resets; pst_timing_read

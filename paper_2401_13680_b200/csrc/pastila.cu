@@ -328,6 +328,27 @@ __global__ void k_colmin(const double* __restrict__ D, int64_t rows, int64_t N, 
   }
 }
 
+// Running per-window minimum over successive row chunks (streamed selection):
+// strict '<' keeps the first (lowest) segment index, chunks arrive in order.
+__global__ void k_colmin_acc(const double* __restrict__ D, int64_t rows, int64_t N, int64_t ld, int64_t base,
+                             double* minval, int32_t* arg) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    double b = minval[j];
+    int64_t bi = -1;
+    for (int64_t r = 0; r < rows; ++r) {
+      const double v = D[r * ld + j];
+      if (v < b) {
+        b = v;
+        bi = r;
+      }
+    }
+    if (bi >= 0) {
+      minval[j] = b;
+      arg[j] = (int32_t)(bi + base);
+    }
+  }
+}
+
 __global__ void k_count(const int32_t* __restrict__ arg, int64_t N, unsigned long long* counts) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
     atomicAdd(&counts[arg[j]], 1ull);
@@ -677,6 +698,62 @@ int pst_colmin_dev(pst_ctx* c, const double* D, int64_t rows, int64_t N, int64_t
 
 static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
                       pst_snippets* res);
+static int run_select_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t n,
+                               int64_t K, int64_t chunk, pst_snippets* res);
+
+// Rows of D that fit the device next to the profile-kernel scratch; the
+// whole S x N matrix when it fits (PASTILA_STREAM_ROWS forces a chunk size).
+static int64_t profile_chunk_rows(pst_ctx* c, int64_t S, int64_t N) {
+  if (const char* e = getenv("PASTILA_STREAM_ROWS")) {
+    const int64_t v = atoll(e);
+    if (v >= 1 && v < S) return v;
+  }
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return S;
+  const size_t have = fr + c->D_bytes;  // D is reallocated in place
+  const size_t reserve = ((size_t)14 << 30) + (size_t)N * 8 * 16;  // kernel scratch (2 x 6 GB) + work buffers
+  if (have <= reserve) return 1;
+  const int64_t rows = (int64_t)((have - reserve) / ((size_t)N * 8));
+  return rows >= S ? S : (rows < 1 ? 1 : rows);
+}
+
+// Profiles of segments [seg_lo, seg_hi) computed chunk by chunk and reduced
+// without keeping them: areas_dev[s - seg_lo] = sum_j min(D[s][j], curve[j])
+// (curve NULL: plain sums); optional running per-window minimum + first
+// argmin (segment index; caller initialises minval to +inf) and running max
+// (caller initialises *rowmax_dev to 0 as unsigned 64-bit bits).
+int pst_profile_reduce_dev(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                           const double* curve_dev, double* areas_dev, double* minval_dev, int32_t* argmin_dev,
+                           double* rowmax_dev) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t S = c->n / m, N = c->n - m + 1;
+  if (seg_lo < 0 || seg_hi > S || seg_lo >= seg_hi) {
+    pst_set_error("segment index %lld out of range [0, %lld)", (long long)(seg_lo < 0 ? seg_lo : seg_hi - 1),
+                  (long long)S);
+    return PST_EINVAL;
+  }
+  int64_t chunk = profile_chunk_rows(c, seg_hi - seg_lo, N);
+  PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)chunk * N * sizeof(double)));
+  for (int64_t s0 = seg_lo; s0 < seg_hi; s0 += chunk) {
+    const int64_t rows = std::min(chunk, seg_hi - s0);
+    PST_TRY(launch_mpdist(c, m, l, k, s0, s0 + rows, c->D, N));
+    k_areas<<<(unsigned)rows, 256, 0, c->st>>>(c->D, N, N, curve_dev, areas_dev + (s0 - seg_lo));
+    c->launches++;
+    if (minval_dev && argmin_dev) {
+      k_colmin_acc<<<grid_for(N, 256), 256, 0, c->st>>>(c->D, rows, N, N, s0, minval_dev, argmin_dev);
+      c->launches++;
+    }
+    if (rowmax_dev) {
+      dim3 g((unsigned)grid_for(N, 256, 64), (unsigned)std::min<int64_t>(rows, 64));
+      k_max<<<g, 256, 0, c->st>>>(c->D, rows, N, N, (unsigned long long*)rowmax_dev);
+      c->launches++;
+    }
+    PST_CUDA(cudaGetLastError());
+  }
+  return PST_OK;
+}
 
 int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res) {
   if (!valid(c)) return PST_EINVAL;
@@ -692,6 +769,8 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
     pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
     return PST_EINVAL;
   }
+  const int64_t chunk = profile_chunk_rows(c, S, N);
+  if (chunk < S) return run_select_streamed(c, m, l, k, S, N, n, K, chunk, res);
   PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)S * N * sizeof(double)));
   PST_TRY(launch_mpdist(c, m, l, k, 0, S, c->D, N));
   return run_select(c, c->D, S, N, n, K, res);
@@ -712,10 +791,16 @@ int pst_select_from_profiles(pst_ctx* c, const double* Dh, int64_t S, int64_t N,
   return run_select(c, c->D, S, N, n, K, res);
 }
 
-static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
-                      pst_snippets* res) {
-  // device buffers: D (S x N), work: curve[N], areas[S], taken[S], best[K], counts[S], nearest[N],
-  // ordered profiles [K x N], labels[n], pair sums, max
+// Device work buffers of one selection.
+struct SelBufs {
+  double *curve, *areas, *prof, *pair, *nearval, *rows;
+  uint8_t* taken;
+  int64_t *best, *labels, *ord, *zero;
+  unsigned long long *counts, *dmax;
+  int32_t* nearest;
+};
+
+static int sel_bufs(pst_ctx* c, int64_t S, int64_t N, int64_t n, int64_t K, bool streamed, SelBufs& b) {
   const int64_t npair = K * (K - 1) / 2;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -725,88 +810,83 @@ static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t
   };
   const size_t o_curve = take(N * 8), o_areas = take(S * 8), o_taken = take(S), o_best = take(K * 8),
                o_counts = take(S * 8), o_near = take(N * 4), o_prof = take(K * N * 8), o_lab = take(n * 8),
-               o_pair = take((npair + 1) * 8), o_max = take(8), o_ord = take(K * 8);
+               o_pair = take((npair + 1) * 8), o_max = take(8), o_ord = take(K * 8), o_zero = take(8),
+               o_nv = streamed ? take(N * 8) : 0, o_rows = streamed ? take(K * N * 8) : 0;
   PST_TRY(pst_ensure(&c->work, &c->work_bytes, off));
   char* wb = (char*)c->work;
-  double* curve = (double*)(wb + o_curve);
-  double* areas = (double*)(wb + o_areas);
-  uint8_t* taken = (uint8_t*)(wb + o_taken);
-  int64_t* best = (int64_t*)(wb + o_best);
-  unsigned long long* counts = (unsigned long long*)(wb + o_counts);
-  int32_t* nearest = (int32_t*)(wb + o_near);
-  double* prof = (double*)(wb + o_prof);
-  int64_t* labels = (int64_t*)(wb + o_lab);
-  double* pair = (double*)(wb + o_pair);
-  unsigned long long* dmax = (unsigned long long*)(wb + o_max);
-  int64_t* ord = (int64_t*)(wb + o_ord);
+  b.curve = (double*)(wb + o_curve);
+  b.areas = (double*)(wb + o_areas);
+  b.taken = (uint8_t*)(wb + o_taken);
+  b.best = (int64_t*)(wb + o_best);
+  b.counts = (unsigned long long*)(wb + o_counts);
+  b.nearest = (int32_t*)(wb + o_near);
+  b.prof = (double*)(wb + o_prof);
+  b.labels = (int64_t*)(wb + o_lab);
+  b.pair = (double*)(wb + o_pair);
+  b.dmax = (unsigned long long*)(wb + o_max);
+  b.ord = (int64_t*)(wb + o_ord);
+  b.zero = (int64_t*)(wb + o_zero);
+  b.nearval = streamed ? (double*)(wb + o_nv) : nullptr;
+  b.rows = streamed ? (double*)(wb + o_rows) : nullptr;
+  return PST_OK;
+}
 
-  // profile_max
-  PST_CUDA(cudaMemsetAsync(dmax, 0, 8, c->st));
-  {
-    dim3 g((unsigned)grid_for(N, 256, 64), (unsigned)std::min<int64_t>(S, 64));
-    k_max<<<g, 256, 0, c->st>>>(D, S, N, N, dmax);
-    c->launches++;
-  }
-  // greedy (snippets.py:201-210)
-  PST_CUDA(cudaMemsetAsync(taken, 0, S, c->st));
-  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(curve, HUGE_VAL, N);
+// Common tail: counts, (-frac, index) ordering, ordered profiles, labels,
+// criterion pair sums, curve area and the host copies.  src/ld/src_row[step]
+// locate the chosen profiles (rows of D, or the streamed row buffer).
+static int finish_select(pst_ctx* c, SelBufs& b, int64_t S, int64_t N, int64_t n, int64_t K, const double* src,
+                         const std::vector<int64_t>& src_row, pst_snippets* res) {
+  const int64_t npair = K * (K - 1) / 2;
+  PST_CUDA(cudaMemsetAsync(b.counts, 0, S * 8, c->st));
+  k_count<<<grid_for(N, 256), 256, 0, c->st>>>(b.nearest, N, b.counts);
   c->launches++;
-  for (int64_t step = 0; step < K; ++step) {
-    k_areas<<<(unsigned)S, 256, 0, c->st>>>(D, N, N, step == 0 ? nullptr : curve, areas);
-    k_pick<<<1, 1024, 0, c->st>>>(areas, taken, S, best + step);
-    k_curve<<<grid_for(N, 256), 256, 0, c->st>>>(curve, D, N, best + step, N);
-    c->launches += 3;
-  }
-  PST_CUDA(cudaGetLastError());
-  // attribution (snippets.py:212-213)
-  PST_CUDA(cudaMemsetAsync(counts, 0, S * 8, c->st));
-  k_colmin<<<grid_for(N, 256), 256, 0, c->st>>>(D, S, N, N, 0, nullptr, nearest);
-  k_count<<<grid_for(N, 256), 256, 0, c->st>>>(nearest, N, counts);
-  c->launches += 2;
   PST_CUDA(cudaGetLastError());
   // host: chosen order by (-frac, index)  (snippets.py:228)
   std::vector<int64_t> chosen(K);
   std::vector<unsigned long long> hcounts(S);
   unsigned long long hmax = 0;
-  PST_CUDA(cudaMemcpyAsync(chosen.data(), best, K * 8, cudaMemcpyDeviceToHost, c->st));
-  PST_CUDA(cudaMemcpyAsync(hcounts.data(), counts, S * 8, cudaMemcpyDeviceToHost, c->st));
-  PST_CUDA(cudaMemcpyAsync(&hmax, dmax, 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(chosen.data(), b.best, K * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(hcounts.data(), b.counts, S * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(&hmax, b.dmax, 8, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
   std::vector<int64_t> order(K);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    const double fa = (double)hcounts[chosen[a]] / (double)N, fb = (double)hcounts[chosen[b]] / (double)N;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t bb) {
+    const double fa = (double)hcounts[chosen[a]] / (double)N, fb = (double)hcounts[chosen[bb]] / (double)N;
     if (fa != fb) return fa > fb;
-    return chosen[a] < chosen[b];
+    return chosen[a] < chosen[bb];
   });
-  std::vector<int64_t> ordidx(K);
-  for (int64_t r = 0; r < K; ++r) ordidx[r] = chosen[order[r]];
-  PST_CUDA(cudaMemcpyAsync(ord, ordidx.data(), K * 8, cudaMemcpyHostToDevice, c->st));
+  std::vector<int64_t> ordidx(K), ordsrc(K);
+  for (int64_t r = 0; r < K; ++r) {
+    ordidx[r] = chosen[order[r]];
+    ordsrc[r] = src_row[order[r]];
+  }
+  PST_CUDA(cudaMemcpyAsync(b.ord, ordsrc.data(), K * 8, cudaMemcpyHostToDevice, c->st));
   {
     dim3 g((unsigned)grid_for(N, 256, 256), (unsigned)K);
-    k_gather_rows<<<g, 256, 0, c->st>>>(D, N, ord, K, N, prof);
+    k_gather_rows<<<g, 256, 0, c->st>>>(src, N, b.ord, K, N, b.prof);
     c->launches++;
   }
   if (res->labels) {
-    k_labels<<<grid_for(n, 256), 256, 0, c->st>>>(prof, K, N, n, labels);
+    k_labels<<<grid_for(n, 256), 256, 0, c->st>>>(b.prof, K, N, n, b.labels);
     c->launches++;
   }
   if (npair > 0) {
-    k_pairdiff<<<(unsigned)npair, 256, 0, c->st>>>(prof, N, K, pair);
+    k_pairdiff<<<(unsigned)npair, 256, 0, c->st>>>(b.prof, N, K, b.pair);
     c->launches++;
   }
   // curve area: deterministic device sum
-  k_areas<<<1, 256, 0, c->st>>>(curve, N, N, nullptr, areas);
+  k_areas<<<1, 256, 0, c->st>>>(b.curve, N, N, nullptr, b.areas);
   c->launches++;
   PST_CUDA(cudaGetLastError());
   double area = 0.0;
   std::vector<double> hpair(npair > 0 ? npair : 1);
-  PST_CUDA(cudaMemcpyAsync(&area, areas, 8, cudaMemcpyDeviceToHost, c->st));
-  if (npair > 0) PST_CUDA(cudaMemcpyAsync(hpair.data(), pair, npair * 8, cudaMemcpyDeviceToHost, c->st));
-  if (res->curve) PST_CUDA(cudaMemcpyAsync(res->curve, curve, N * 8, cudaMemcpyDeviceToHost, c->st));
-  if (res->profiles) PST_CUDA(cudaMemcpyAsync(res->profiles, prof, K * N * 8, cudaMemcpyDeviceToHost, c->st));
-  if (res->nearest) PST_CUDA(cudaMemcpyAsync(res->nearest, nearest, N * 4, cudaMemcpyDeviceToHost, c->st));
-  if (res->labels) PST_CUDA(cudaMemcpyAsync(res->labels, labels, n * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(&area, b.areas, 8, cudaMemcpyDeviceToHost, c->st));
+  if (npair > 0) PST_CUDA(cudaMemcpyAsync(hpair.data(), b.pair, npair * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->curve) PST_CUDA(cudaMemcpyAsync(res->curve, b.curve, N * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->profiles) PST_CUDA(cudaMemcpyAsync(res->profiles, b.prof, K * N * 8, cudaMemcpyDeviceToHost, c->st));
+  if (res->nearest) PST_CUDA(cudaMemcpyAsync(res->nearest, b.nearest, N * 4, cudaMemcpyDeviceToHost, c->st));
+  if (res->labels) PST_CUDA(cudaMemcpyAsync(res->labels, b.labels, n * 8, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
   res->profile_area = area;
   double pm;
@@ -825,6 +905,75 @@ static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t
     for (int64_t s = 0; s < S; ++s) res->counts[s] = (int64_t)hcounts[s];
   res->unassigned = N - covered;
   return PST_OK;
+}
+
+// Greedy + attribution on the resident S x N matrix D.
+static int run_select(pst_ctx* c, const double* D, int64_t S, int64_t N, int64_t n, int64_t K,
+                      pst_snippets* res) {
+  SelBufs b;
+  PST_TRY(sel_bufs(c, S, N, n, K, false, b));
+  // profile_max
+  PST_CUDA(cudaMemsetAsync(b.dmax, 0, 8, c->st));
+  {
+    dim3 g((unsigned)grid_for(N, 256, 64), (unsigned)std::min<int64_t>(S, 64));
+    k_max<<<g, 256, 0, c->st>>>(D, S, N, N, b.dmax);
+    c->launches++;
+  }
+  // greedy (snippets.py:201-210)
+  PST_CUDA(cudaMemsetAsync(b.taken, 0, S, c->st));
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, HUGE_VAL, N);
+  c->launches++;
+  for (int64_t step = 0; step < K; ++step) {
+    k_areas<<<(unsigned)S, 256, 0, c->st>>>(D, N, N, step == 0 ? nullptr : b.curve, b.areas);
+    k_pick<<<1, 1024, 0, c->st>>>(b.areas, b.taken, S, b.best + step);
+    k_curve<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, D, N, b.best + step, N);
+    c->launches += 3;
+  }
+  PST_CUDA(cudaGetLastError());
+  // attribution (snippets.py:212-213)
+  k_colmin<<<grid_for(N, 256), 256, 0, c->st>>>(D, S, N, N, 0, nullptr, b.nearest);
+  c->launches++;
+  std::vector<int64_t> chosen(K);
+  PST_CUDA(cudaMemcpyAsync(chosen.data(), b.best, K * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return finish_select(c, b, S, N, n, K, D, chosen, res);
+}
+
+// Same greedy when S x N does not fit the device (C4: n = 1e7): profiles are
+// recomputed chunk by chunk for every greedy round and reduced on the fly
+// (pst_profile_reduce_dev); only the K chosen rows are kept.  The first pass
+// also produces the attribution minima and profile_max.  Profiles do not
+// depend on the chunking, so the result is identical to the resident path.
+static int run_select_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t n,
+                               int64_t K, int64_t chunk, pst_snippets* res) {
+  (void)chunk;
+  SelBufs b;
+  PST_TRY(sel_bufs(c, S, N, n, K, true, b));
+  PST_CUDA(cudaMemsetAsync(b.dmax, 0, 8, c->st));
+  PST_CUDA(cudaMemsetAsync(b.taken, 0, S, c->st));
+  PST_CUDA(cudaMemsetAsync(b.zero, 0, 8, c->st));
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, HUGE_VAL, N);
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(b.nearval, HUGE_VAL, N);
+  c->launches += 2;
+  std::vector<int64_t> steps(K);
+  for (int64_t step = 0; step < K; ++step) {
+    if (step == 0)
+      PST_TRY(pst_profile_reduce_dev(c, m, l, k, 0, S, nullptr, b.areas, b.nearval, b.nearest, (double*)b.dmax));
+    else
+      PST_TRY(pst_profile_reduce_dev(c, m, l, k, 0, S, b.curve, b.areas, nullptr, nullptr, nullptr));
+    k_pick<<<1, 1024, 0, c->st>>>(b.areas, b.taken, S, b.best + step);
+    c->launches++;
+    int64_t best = 0;
+    PST_CUDA(cudaMemcpyAsync(&best, b.best + step, 8, cudaMemcpyDeviceToHost, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));
+    double* row = b.rows + step * N;
+    PST_TRY(launch_mpdist(c, m, l, k, best, best + 1, row, N));  // the chosen profile, recomputed
+    k_curve<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, row, N, b.zero, N);
+    c->launches++;
+    PST_CUDA(cudaGetLastError());
+    steps[step] = step;
+  }
+  return finish_select(c, b, S, N, n, K, b.rows, steps, res);
 }
 
 // criterion_score on caller-supplied profiles (length_select.py:56-87):

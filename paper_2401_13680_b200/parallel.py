@@ -109,6 +109,7 @@ class ShardedSearch:
         dist = _dist()
         ws = world_size()
         chosen: list[int] = []
+        self.chosen_rows = []  # profiles of the chosen segments, in greedy order
         curve = None
         for _ in range(K):
             # local best (lowest index among equal areas), then global (area, index) minimum
@@ -132,6 +133,7 @@ class ShardedSearch:
             rt = self.to_dev(np.ascontiguousarray(row, dtype=np.float64))
             dist.broadcast(rt, src=owner)
             row = self.from_dev(rt)
+            self.chosen_rows.append(np.array(row, dtype=np.float64, copy=True))
             curve = row.copy() if curve is None else np.minimum(curve, row)
         # nearest segment per window: MIN over values, then MIN over indices among ties
         mv, ma = self.b.colmin()
@@ -201,6 +203,129 @@ class DeviceRows:
 
     def rowmax(self):
         return float(self.D.max().item()) if self.rows else 0.0
+
+
+class StreamedRows:
+    """ShardedSearch backend for rank-local segment rows that do not fit HBM
+    (C4: n = 1e7, 39,062 segments of 1e7 windows = 3.1 TB): every areas() call
+    recomputes the rank's profiles in device-sized chunks and reduces them on
+    the fly (pst_profile_reduce_dev); the first call also yields the
+    per-window minima and the row max, row(i) recomputes one profile.  Same
+    values as DeviceRows (profiles do not depend on the chunking)."""
+
+    def __init__(self, series, params, seg_lo: int, seg_hi: int):
+        import ctypes as C
+
+        import torch
+
+        from . import _native
+
+        self.C, self.torch = C, torch
+        self.ctx = _native.context()
+        self.ctx.set_series(series.values)
+        self.dev = torch.device("cuda", self.ctx.device)
+        self.p = params
+        self.lo, self.hi = seg_lo, seg_hi
+        self.N = series.n - params.snippet_size + 1
+        self.rows = seg_hi - seg_lo
+        self._colmin = None
+        self._rowmax = None
+
+    def _mkl(self):
+        return int(self.p.snippet_size), int(self.p.window_size), int(self.p.k)
+
+    def areas(self, curve):
+        torch, C = self.torch, self.C
+        out = torch.empty(self.rows, dtype=torch.float64, device=self.dev)
+        if self.rows == 0:
+            self._colmin = (np.full(self.N, np.inf), np.zeros(self.N, dtype=np.int64))
+            self._rowmax = 0.0
+            return out.cpu().numpy()
+        cptr = mv = ma = mx = None
+        if curve is not None:
+            ct = torch.as_tensor(curve, dtype=torch.float64, device=self.dev)
+            cptr = C.c_void_p(ct.data_ptr())
+        first = self._colmin is None
+        if first:
+            mvt = torch.full((self.N,), float("inf"), dtype=torch.float64, device=self.dev)
+            mat = torch.zeros(self.N, dtype=torch.int32, device=self.dev)
+            mxt = torch.zeros(1, dtype=torch.float64, device=self.dev)
+            mv, ma, mx = (C.c_void_p(t.data_ptr()) for t in (mvt, mat, mxt))
+        self.ctx.call("pst_profile_reduce_dev", *self._mkl(), self.lo, self.hi, cptr,
+                      C.c_void_p(out.data_ptr()), mv, ma, mx)
+        self.ctx.call("pst_sync")
+        if first:
+            self._colmin = (mvt.cpu().numpy(), mat.cpu().numpy().astype(np.int64) - self.lo)
+            self._rowmax = float(mxt.item())
+        return out.cpu().numpy()
+
+    def row(self, i):
+        torch, C = self.torch, self.C
+        r = torch.empty((1, self.N), dtype=torch.float64, device=self.dev)
+        s = self.lo + int(i)
+        self.ctx.call("pst_profiles_dev", *self._mkl(), s, s + 1, C.c_void_p(r.data_ptr()), C.c_int64(self.N))
+        self.ctx.call("pst_sync")
+        return r[0].cpu().numpy()
+
+    def colmin(self):
+        if self._colmin is None:
+            self.areas(None)
+        return self._colmin
+
+    def rowmax(self):
+        if self._rowmax is None:
+            self.areas(None)
+        return self._rowmax if self.rows else 0.0
+
+
+def select_snippets_sharded(series, params, num_snippets: int, *, backend=None):
+    """``select_snippets`` for ONE length with its segment rows sharded over the
+    ranks of the default process group: rank r owns a
+    contiguous segment range, keeps its profiles in HBM when they fit
+    (DeviceRows) or recomputes them per greedy round (StreamedRows), and the
+    ranks combine through ShardedSearch (NCCL on GPUs, gloo in CPU tests).
+    Every rank returns the same SnippetResult as the single-GPU call."""
+    import torch
+
+    from .mpdist import MPdistProfile
+    from .snippets import Snippet, SnippetResult, segment
+
+    segs = segment(series, params.snippet_size)
+    S, K, n, m = segs.count, int(num_snippets), series.n, params.snippet_size
+    if not 1 <= K <= S:
+        raise ValueError(f"snippet count {K} out of range [1, {S}]")
+    N = n - m + 1
+    ranges = segment_ranges(S, world_size())
+    lo, hi = ranges[rank()]
+    if backend is None:
+        from . import _native
+
+        dev = _native.context().device
+        free = torch.cuda.mem_get_info(dev)[0]
+        fits = (hi - lo) * N * 8 + (16 << 30) < free
+        backend = (DeviceRows if fits else StreamedRows)(series, params, lo, hi)
+    d = _dist()
+    on_gpu = d is not None and d.get_backend() == "nccl"
+    tdev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+
+    def to_dev(a):
+        return torch.as_tensor(np.ascontiguousarray(a)).to(tdev)
+
+    def from_dev(t):
+        return t.cpu().numpy()
+
+    ss = ShardedSearch(backend, ranges, N, to_dev, from_dev)
+    chosen, curve, nearest, pmax = ss.run(K)
+    counts = np.bincount(nearest, minlength=S).astype(np.int64)
+    order = sorted(range(K), key=lambda r: (-(counts[chosen[r]] / N), chosen[r]))  # snippets.py:228
+    snippets = tuple(Snippet(index=int(chosen[r]), start=int(chosen[r]) * m, length=m,
+                             frac=float(counts[chosen[r]] / N),
+                             neighbors=np.flatnonzero(nearest == chosen[r]).astype(np.int64)) for r in order)
+    profiles = tuple(MPdistProfile(segment_index=int(chosen[r]), values=ss.chosen_rows[r]) for r in order)
+    return SnippetResult(
+        snippet_size=m, window_size=params.window_size, k=params.k, series_length=n, snippets=snippets,
+        curve=curve, profile_area=float(np.asarray(curve).sum()), profiles=profiles, profile_max=float(pmax),
+        segment_window_counts=counts, unassigned_windows=int(N - sum(counts[c] for c in chosen)))
 
 
 def timed(fn, *a, **kw):

@@ -91,6 +91,25 @@ def _worker_lengths(rank, ws, port, out):
     dist.destroy_process_group()
 
 
+def _worker_sharded_api(rank, ws, port, out):
+    """public entry point (parallel.select_snippets_sharded) with an oracle backend"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import paper_2401_13680_b200 as P
+    from paper_2401_13680_b200 import parallel
+
+    x = _series()
+    m, K = 40, 3
+    D = O.all_profiles(x, m, O.window_default(m), O.order_default(m))
+    lo, hi = parallel.segment_ranges(D.shape[0], ws)[rank]
+    r = parallel.select_snippets_sharded(P.TimeSeries(x), P.MPdistParams(m), K, backend=OracleRows(D[lo:hi]))
+    if rank == 0:
+        out.put(([s.index for s in r.snippets], [s.frac for s in r.snippets],
+                 [s.neighbors.tolist() for s in r.snippets], r.curve, np.vstack([p.values for p in r.profiles]),
+                 r.profile_max, r.segment_window_counts, r.unassigned_windows))
+    dist.destroy_process_group()
+
+
 def _spawn(fn):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -129,3 +148,14 @@ def test_partitions_cover_work():
     assert parallel.segment_ranges(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
     parts = parallel.length_partition([5.0, 4.0, 3.0, 3.0, 1.0], 8)
     assert sorted(i for p in parts for i in p) == [0, 1, 2, 3, 4] and len(parts) == 8
+
+
+def test_sharded_select_api_matches_oracle():
+    idx, fracs, neigh, curve, prof, pmax, counts, unassigned = _spawn(_worker_sharded_api)
+    ref = O.select_snippets(_series(), 40, 3)
+    assert idx == ref["indices"] and fracs == ref["fracs"]
+    assert neigh == [a.tolist() for a in ref["neighbors"]]
+    np.testing.assert_array_equal(curve, ref["curve"])
+    np.testing.assert_array_equal(prof, ref["profiles"])
+    assert pmax == ref["profile_max"] and unassigned == ref["unassigned_windows"]
+    np.testing.assert_array_equal(counts, ref["counts"])

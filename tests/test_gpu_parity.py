@@ -97,12 +97,12 @@ def test_mpdist_random_vs_oracle(seed):
         np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
 
 
-@pytest.mark.parametrize("m", [24, 48, 80, 96, 97, 160, 161, 288, 289, 600, 1100])
+@pytest.mark.parametrize("m", [24, 48, 80, 96, 97, 160, 161, 288, 289, 600, 1100, 2048, 4096])
 def test_mpdist_window_classes_vs_oracle(m):
     """Every register class boundary of the row / selection kernels and the
     long-window paths (w > 288 shared-memory van Herk, w > 512 gather selection)."""
     rng = np.random.default_rng(m)
-    n = max(6 * m, 1500)
+    n = max(6 * m, 1500) if m <= 1100 else 3 * m + 777  # C5 window sizes: w = 1025, 2049
     x = np.cumsum(rng.standard_normal(n)) * 0.1 + np.sin(np.arange(n) * 2 * np.pi / 37)
     params = P.MPdistParams(m)
     st = O.sliding_stats(x, params.window_size)

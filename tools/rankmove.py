@@ -27,4 +27,4 @@ for m in [int(a) for a in sys.argv[1].split(',')]:
         moves.append(mv)
     mv = np.concatenate(moves)
     a = np.abs(mv)
-    print(f"m={m} w={w} k={k}: 0:{(a==0).mean():.3f} <=1:{(a<=1).mean():.3f} <=2:{(a<=2).mean():.3f} <=3:{(a<=3).mean():.3f} <=4:{(a<=4).mean():.3f} max {a.max()}")
+    print(f"m={m} w={w} k={k}: " + " ".join(f"<={t}:{(a<=t).mean():.3f}" for t in (0,1,2,3,4,6,8,12,16)) + f" max {a.max()}")

@@ -352,12 +352,23 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
-  double* xs = sm;             // [l]
-  double* edge = xs + l;       // [w]
-  double* rdf = edge + w;      // [w] df[q-1] per row
-  double* rdg = rdf + w;       // [w] dg[q-1] per row
-  double* rnq = rdg + w;       // [w] nrm[q] per row
-  double* E0 = rnq + w;        // [NCmax] row e-values (even rows), later allP_BA
+  // Long windows (CHM == 0, shared-memory van Herk) keep only edge[] of the
+  // per-row arrays in shared memory -- their row scalars come from global
+  // memory (L1 broadcast) -- and stage xs in E1 (unused until row 1), so a
+  // tile can hold P = 7 columns per thread.
+  constexpr bool kLong = (CHM == 0);
+  double *xs, *edge, *rdf = nullptr, *rdg = nullptr, *rnq = nullptr, *E0;
+  if constexpr (!kLong) {
+    xs = sm;                   // [l]
+    edge = xs + l;             // [w]
+    rdf = edge + w;            // [w] df[q-1] per row
+    rdg = rdf + w;             // [w] dg[q-1] per row
+    rnq = rdg + w;             // [w] nrm[q] per row
+    E0 = rnq + w;              // [NCmax] row e-values (even rows), later allP_BA
+  } else {
+    edge = sm;
+    E0 = edge + w;
+  }
   double* E1 = E0 + NCmax;     // [NCmax] row e-values (odd rows)
   double* xfer = E1 + NCmax;   // [64]
   double* red = xfer + 64;     // [2]
@@ -365,6 +376,7 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   double* SR1 = SR0 + NCmax;    // [NCmax] AB row buffer (odd rows)
   double* SUF = SR1 + NCmax;    // [NCmax] (shared-memory van Herk only)
   double* PRE = SUF + NCmax;    // [NCmax]
+  if constexpr (kLong) xs = (l <= NCmax) ? E1 : PRE + NCmax;
   double* E = E0;
   // AB scratch of this CTA: [w][Tp], each row in lane-run order (store_ab_row)
   const int R = (int)a.R, Tp = (int)a.Tp;
@@ -421,10 +433,12 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
       edge[i] = fma(-muQ[i], sx, acc);
     }
   }
-  for (int i = tid; i < w; i += NT) {
-    rdf[i] = i > 0 ? a.df[q0 + i - 1] : 0.0;
-    rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
-    rnq[i] = a.nrm[q0 + i];
+  if constexpr (!kLong) {
+    for (int i = tid; i < w; i += NT) {
+      rdf[i] = i > 0 ? a.df[q0 + i - 1] : 0.0;
+      rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
+      rnq[i] = a.nrm[q0 + i];
+    }
   }
   // ---- per-column constants
   double dgc[P], dfc[P], nrmc[P], bic[P], colmin[P];
@@ -459,14 +473,15 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   for (int i = 0; i < w; ++i) {
     double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
     if (i > 0) {
-      const double dfq = rdf[i], dgq = rdg[i];
+      const double dfq = kLong ? __ldg(a.df + q0 + i - 1) : rdf[i];
+      const double dgq = kLong ? __ldg(a.dg + q0 + i - 1) : rdg[i];
       if (lane == 0 && warp > 0) left = xfer[((i - 1) & 1) * 32 + warp - 1];
 #pragma unroll
       for (int p = P - 1; p >= 1; --p) cov[p] = fma(dfq, dgc[p], fma(dgq, dfc[p], cov[p - 1]));
       cov[0] = (tid == 0) ? edge[i] : fma(dfq, dgc[0], fma(dgq, dfc[0], left));
     }
     if (lane == 31) xfer[(i & 1) * 32 + warp] = cov[P - 1];
-    const double nq = rnq[i];
+    const double nq = kLong ? __ldg(a.nrm + q0 + i) : rnq[i];
     E = (i & 1) ? E1 : E0;
     double* Et = E + tid * P;
     if (nq != 0.0) {
@@ -860,7 +875,7 @@ __device__ __forceinline__ double e_to_dist(double ev, double twol) {
 template <int TM>
 __device__ __forceinline__ double solve_window(const double* __restrict__ ab, const double* BA, int w, int k,
                                                int R, int Tp, int L, int r, int lane, bool fresh, double piv,
-                                               int lt0, int le0, int& ltB, int& leB) {
+                                               int lt0, int le0, int& ltB, int& leB, double* colbuf) {
   const double* Ac = ab + r * 32 + L;
   const double* Bc = BA + L * R + r;
   double x;
@@ -881,14 +896,18 @@ __device__ __forceinline__ double solve_window(const double* __restrict__ ab, co
       b1 += v.b[t] < x;
       b2 += v.b[t] <= x;
     }
-  } else {
-    MemWin v{Ac, Bc, w, (int64_t)Tp};
-    if (fresh) piv = dmax(warp_max(lane < w ? __ldg(Ac + (int64_t)lane * Tp) : -PST_INF) * 0.25, 0.0);
+  } else {  // long windows: the gathered column is staged once in the warp's shared buffer
+#pragma unroll 8
+    for (int i = lane; i < w; i += 32) colbuf[i] = __ldg(Ac + (int64_t)i * Tp);
+    __syncwarp();
+    MemWin v{colbuf, Bc, w, 1};
+    if (fresh) piv = dmax(warp_max(lane < w ? colbuf[lane] : -PST_INF) * 0.25, 0.0);
     x = warp_select_mem(v, lane, k, piv, lt0, le0);
     for (int i = lane; i < w; i += 32) {
       b1 += Bc[i] < x;
       b2 += Bc[i] <= x;
     }
+    __syncwarp();  // colbuf is rewritten by the next solve
   }
   ltB = __reduce_add_sync(FULLMASK, b1);
   leB = __reduce_add_sync(FULLMASK, b2);
@@ -907,6 +926,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
   const double* __restrict__ ab = a.ab + cta * ((int64_t)w * Tp);
   const double* __restrict__ bag = a.ba + cta * NCmax;
   double* BA = smb;
+  double* colbuf = smb + NCmax + warp * w;  // [w] per warp, long windows (TM == 0) only
   for (int c = tid; c < NC; c += NWS * 32) BA[c] = bag[c];
   __syncthreads();
   const double twol = 2.0 * (double)a.l;
@@ -940,7 +960,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
     for (int L = 0; L < 32; ++L) {
       if (L * R + r0 >= NJ) break;  // warp-uniform
       int b1, b2;
-      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2);
+      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2, colbuf);
       if (lane == L) {
         p = prev;
         ltB = b1;
@@ -977,7 +997,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
       const double pl = __shfl_sync(FULLMASK, p, L);
       const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
       int b1, b2;
-      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1, b2);
+      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1, b2, colbuf);
       if (lane == L) {
         p = x;
         ltB = b1;
@@ -1004,7 +1024,7 @@ int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
 
 template <int NWS, int TM>
 int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
-  const size_t smem = (size_t)NCmax * sizeof(double);
+  const size_t smem = (size_t)(NCmax + (TM == 0 ? NWS * a.w : 0)) * sizeof(double);
   auto kern = k_select_run<NWS, TM>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1119,8 +1139,11 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
     const int64_t ncm = (int64_t)tt * pp;
-    return (size_t)(l + 4 * w + ncm * (chm ? 4 : 6) + 64 + 2) * sizeof(double);
+    if (chm == 0)  // long-window layout (k_mpdist kLong): edge + 6 rows (+ xs if it does not fit E1)
+      return (size_t)(w + ncm * 6 + 64 + 2 + (l > ncm ? l : 0)) * sizeof(double);
+    return (size_t)(l + 4 * w + ncm * 4 + 64 + 2) * sizeof(double);
   };
+  if (chm == 0 && smem_for(7, nt) <= smax) P = 7;  // long windows: wider tiles (less halo)
   if (const char* e = getenv("PASTILA_P")) { const int v = atoi(e); if (v == 3 || v == 5) P = v; }  // tuning
   while (P > 1 && smem_for(P, nt) > smax) P -= 2;
   if (smem_for(P, nt) > smax || (int64_t)nt * P < w) {

@@ -1,12 +1,14 @@
 """Attribute ncu SASS-level samples / executed instructions to CUDA source lines.
 
-usage: python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> [top]
+usage: python tools/ncu_lines.py <report.ncu-rep> <kernel-regex> [top] [opcode-regex]
+(with an opcode regex, e.g. "IMAD|FSEL", also prints that opcode class's share per line)
 Needs the .so compiled with -lineinfo (it is) and nvdisasm/cuobjdump in PATH.
 """
 import csv, io, re, subprocess, sys, collections, tempfile, os
 
 rep, kre = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+opre = re.compile(sys.argv[4]) if len(sys.argv) > 4 else None
 so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2401_13680_b200", "libpastila.so")
 out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + kre, "-c", "1", "--page", "source", "--csv",
                       "--print-source", "sass"], capture_output=True, text=True).stdout
@@ -54,7 +56,7 @@ for f in cands:
     if best is None or abs(n - len(sass)) < abs(best[1] - len(sass)):
         best = (f, n)
 f = best[0]
-agg = collections.defaultdict(lambda: [0, 0])
+agg = collections.defaultdict(lambda: [0, 0, 0])
 tot_w = sum(s[1] for s in sass) or 1
 tot_e = sum(s[2] for s in sass) or 1
 base = sass[0][0]
@@ -62,11 +64,17 @@ for i, (a, w, e, src) in enumerate(sass):
     key = addr2line.get((f, a - base), ("?", -1))
     agg[key][0] += w
     agg[key][1] += e
+    if opre is not None:
+        t = src.strip().split()
+        op = (t[1] if t and t[0].startswith("@") and len(t) > 1 else (t[0] if t else ""))
+        if opre.search(op):
+            agg[key][2] += e
 print(f"kernel {kname}  ({len(sass)} SASS instrs; function {f})")
 srcfile = {}
-for (fn, ln), (w, e) in sorted(agg.items(), key=lambda t: -t[1][0])[:top]:
+for (fn, ln), (w, e, oe) in sorted(agg.items(), key=lambda t: -(t[1][2] if opre is not None else t[1][0]))[:top]:
     if fn not in srcfile:
         p = os.path.join(os.path.dirname(so), "csrc", fn)
         srcfile[fn] = open(p).read().splitlines() if os.path.exists(p) else []
     text = srcfile[fn][ln - 1].strip() if 0 < ln <= len(srcfile[fn]) else ""
-    print(f"{100*w/tot_w:5.1f}% stall {100*e/tot_e:5.1f}% inst  {fn}:{ln:<4d} {text[:90]}")
+    extra = f" {100*oe/tot_e:5.1f}% op" if opre is not None else ""
+    print(f"{100*w/tot_w:5.1f}% stall {100*e/tot_e:5.1f}% inst{extra}  {fn}:{ln:<4d} {text[:90]}")

@@ -341,6 +341,99 @@ __device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double
   }
 }
 
+// ---- long windows: van Herk with every block split over several warps ----
+// Scans per row: the suffix minima SUF of blocks 0..nblk-1 and the prefix
+// minima PRE of blocks 0..nblk (block b = columns [b*w, (b+1)*w) of the tile,
+// clipped to NC).  Each scan is cut into Q parts; a warp scans one part
+// (phase 1: part-local scan + part total), and after a barrier adds the carry
+// from the other parts' totals (phase 2).  The window combine
+// AB[j] = min(SUF[j], PRE[j+w-1]) happens when the row is stored (PRE of
+// block b ends in min(block b) = SUF_b[b*w], so u = 0 needs no special case).
+struct SplitGeom {
+  int nblk, Q, L, ntask;  // L = part length
+};
+__device__ __forceinline__ void split_task(const SplitGeom& sg, int t, int w, int NC, bool& suf, int& b, int& q,
+                                           int& lo, int& hi) {
+  const int nS = sg.nblk * sg.Q;
+  suf = t < nS;
+  const int tt = suf ? t : t - nS;
+  b = tt / sg.Q;
+  q = tt - b * sg.Q;
+  const int bb = b * w;
+  const int end = min(bb + w, NC);
+  lo = min(bb + q * sg.L, end);
+  hi = min(lo + sg.L, end);
+}
+// phase 1: part-local scans; TOT[(suf ? 0 : 1) * 32 * 16 + b * 16 + q] = part minimum
+__device__ __forceinline__ void vh_split_scan(const double* __restrict__ E, double* __restrict__ SUF,
+                                              double* __restrict__ PRE, double* __restrict__ TOT,
+                                              const SplitGeom& sg, int w, int NC, int warp, int lane, int nw) {
+  for (int t = warp; t < sg.ntask; t += nw) {
+    bool suf;
+    int b, q, lo, hi;
+    split_task(sg, t, w, NC, suf, b, q, lo, hi);
+    const int len = hi - lo;
+    const int ch = (len + 31) >> 5;
+    const int u0 = lo + lane * ch, u1 = min(u0 + ch, hi);
+    double run = PST_INF;
+    if (suf) {
+      for (int c = u1 - 1; c >= u0; --c) {
+        run = dmin(run, E[c]);
+        SUF[c] = run;
+      }
+    } else {
+      for (int c = u0; c < u1; ++c) {
+        run = dmin(run, E[c]);
+        PRE[c] = run;
+      }
+    }
+    double tot = run;  // carry between lanes of the part
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double o = suf ? __shfl_down_sync(FULLMASK, tot, off) : __shfl_up_sync(FULLMASK, tot, off);
+      if (suf ? lane + off < 32 : lane >= off) tot = dmin(tot, o);
+    }
+    double carry = suf ? __shfl_down_sync(FULLMASK, tot, 1) : __shfl_up_sync(FULLMASK, tot, 1);
+    if (suf ? lane == 31 : lane == 0) carry = PST_INF;
+    if (suf)
+      for (int c = u0; c < u1; ++c) SUF[c] = dmin(SUF[c], carry);
+    else
+      for (int c = u0; c < u1; ++c) PRE[c] = dmin(PRE[c], carry);
+    // part minimum: lane 0 holds the suffix over the whole part, lane 31 the prefix
+    const double pm = __shfl_sync(FULLMASK, tot, suf ? 0 : 31);
+    if (lane == 0) TOT[(suf ? 0 : 512) + b * 16 + q] = pm;
+  }
+}
+// phase 2: carries from the other parts of the same block
+__device__ __forceinline__ void vh_split_carry(double* __restrict__ SUF, double* __restrict__ PRE,
+                                               const double* __restrict__ TOT, const SplitGeom& sg, int w, int NC,
+                                               int warp, int lane, int nw) {
+  for (int t = warp; t < sg.ntask; t += nw) {
+    bool suf;
+    int b, q, lo, hi;
+    split_task(sg, t, w, NC, suf, b, q, lo, hi);
+    if (suf ? q == sg.Q - 1 : q == 0) continue;  // no parts beyond (SUF) / before (PRE)
+    double v = PST_INF;
+    if (lane < sg.Q && (suf ? lane > q : lane < q)) v = TOT[(suf ? 0 : 512) + b * 16 + lane];
+    const double carry = warp_min(v);
+    if (suf)
+      for (int c = lo + lane; c < hi; c += 32) SUF[c] = dmin(SUF[c], carry);
+    else
+      for (int c = lo + lane; c < hi; c += 32) PRE[c] = dmin(PRE[c], carry);
+  }
+}
+// deferred store of a long-window row: AB[j] = min(SUF[j], PRE[j + w - 1]) in lane-run order
+template <int NT, int MAXC>
+__device__ __forceinline__ void store_ab_combine(const AbStore& g, const double* __restrict__ SUF,
+                                                 const double* __restrict__ PREw, double* __restrict__ dst) {
+  const double* s = SUF + g.src;
+  const double* p = PREw + g.src;
+  double* d = dst + g.dst;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+    if (c < g.cnt) d[c * NT] = dmin(s[c * (NT / 32)], p[c * (NT / 32)]);
+}
+
 template <int P, int NT, int CHM>
 __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist(const MPArgs a) {
   extern __shared__ double sm[];
@@ -376,7 +469,8 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   double* SR1 = SR0 + NCmax;    // [NCmax] AB row buffer (odd rows)
   double* SUF = SR1 + NCmax;    // [NCmax] (shared-memory van Herk only)
   double* PRE = SUF + NCmax;    // [NCmax]
-  if constexpr (kLong) xs = (l <= NCmax) ? E1 : PRE + NCmax;
+  double* TOT = PRE + NCmax;    // [1024] part minima of the split van Herk (long windows)
+  if constexpr (kLong) xs = (l <= NCmax) ? E1 : TOT + 1024;
   double* E = E0;
   // AB scratch of this CTA: [w][Tp], each row in lane-run order (store_ab_row)
   const int R = (int)a.R, Tp = (int)a.Tp;
@@ -470,6 +564,14 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
   }
   const bool tail = (tid + 1) * P > NC;  // this thread owns columns past the tile's last one
   const AbStore abst = ab_store_setup<NT>(NJ, R, tid);
+  SplitGeom sg;
+  {
+    sg.nblk = (NJ + w - 1) / w;
+    const int scans = 2 * sg.nblk + 1;
+    sg.Q = max(1, min(16, NW / scans));
+    sg.L = (w + sg.Q - 1) / sg.Q;
+    sg.ntask = scans * sg.Q;
+  }
   for (int i = 0; i < w; ++i) {
     double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
     if (i > 0) {
@@ -511,20 +613,33 @@ __global__ void __launch_bounds__(NT, (P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <=
       if (ql >= 0 && ql < P) Et[ql] = 0.0;
     }
     __syncthreads();
-    // the previous row's AB values are complete (written before this barrier)
-    if (i > 0) store_ab_row<NT, P + 1>(abst, (i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp);
-    double* srow = (i & 1) ? SR1 : SR0;
-    if constexpr (CHM > 0)
-      vh_row_reg<CHM>(E, w, g, warp, NW, srow);
-    else {
-      vh_row_smem(E, SUF, PRE, NC, NJ, w, warp, lane, NW, srow);
-      __syncthreads();  // SUF/PRE reused next row
+    if constexpr (CHM > 0) {
+      // the previous row's AB values are complete (written before this barrier)
+      if (i > 0) store_ab_row<NT, P + 1>(abst, (i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp);
+      vh_row_reg<CHM>(E, w, g, warp, NW, (i & 1) ? SR1 : SR0);
+    } else {
+      // buffers by row parity: (SUF, PRE) = (SUF, PRE) for even rows, (SR0, SR1) for odd rows
+      if (i > 0) {
+        const bool po = (i - 1) & 1;
+        store_ab_combine<NT, P + 1>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1), ab + (int64_t)(i - 1) * Tp);
+      }
+      double* sufc = (i & 1) ? SR0 : SUF;
+      double* prec = (i & 1) ? SR1 : PRE;
+      vh_split_scan(E, sufc, prec, TOT, sg, w, NC, warp, lane, NW);
+      __syncthreads();  // part totals complete
+      vh_split_carry(sufc, prec, TOT, sg, w, NC, warp, lane, NW);
     }
-    // no trailing barrier: the next row writes the other E / row buffer; the
+    // no trailing barrier: the next row writes the other E / row buffers; the
     // barrier after that row's writes orders this row's reads before row i+2's writes.
+    // (TOT is rewritten only after the next row's first barrier.)
   }
   __syncthreads();
-  store_ab_row<NT, P + 1>(abst, ((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp);
+  if constexpr (CHM > 0) {
+    store_ab_row<NT, P + 1>(abst, ((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp);
+  } else {
+    const bool po = (w - 1) & 1;
+    store_ab_combine<NT, P + 1>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1), ab + (int64_t)(w - 1) * Tp);
+  }
   E = E0;
 
   // ---- allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
@@ -1135,12 +1250,13 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   if (const char* e = getenv("PASTILA_CHM")) {  // tuning experiments
     const int v = atoi(e);
     if ((v == 3 || v == 5 || v == 9) && 32 * v >= w) chm = v;
+    if (v == 0) chm = 0;  // split shared-memory van Herk
   }
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   auto smem_for = [&](int pp, int tt) {
     const int64_t ncm = (int64_t)tt * pp;
-    if (chm == 0)  // long-window layout (k_mpdist kLong): edge + 6 rows (+ xs if it does not fit E1)
-      return (size_t)(w + ncm * 6 + 64 + 2 + (l > ncm ? l : 0)) * sizeof(double);
+    if (chm == 0)  // long-window layout (k_mpdist kLong): edge + 6 rows + part minima (+ xs if not in E1)
+      return (size_t)(w + ncm * 6 + 64 + 2 + 1024 + (l > ncm ? l : 0)) * sizeof(double);
     return (size_t)(l + 4 * w + ncm * 4 + 64 + 2) * sizeof(double);
   };
   if (chm == 0 && smem_for(7, nt) <= smax) P = 7;  // long windows: wider tiles (less halo)

@@ -10,8 +10,11 @@ default_cost, scheduler.py:90-102).  Metric: pairs/s (whole job).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pastila|reference]
 
-N>1: launched by torchrun (one process per GPU); lengths are sharded by
-Karmarkar-Karp over ranks (weak... strong scaling: the total work is fixed).
+N>1: launched by torchrun (one process per GPU), strong scaling (the total
+work is fixed).  Default --shard rows: every length's segment rows are split
+evenly over the ranks (parallel.select_snippets_sharded: per greedy step one
+(area, index) all-gather + one profile broadcast over NCCL), so every rank has
+1/N of every length.  --shard lengths: Karmarkar-Karp over whole lengths.
 Timing: barrier + synchronize, CUDA events on the library stream, max over
 ranks.  Inputs (8 MB) are far smaller than L2 and are re-derived inside the
 step (prefix sums recomputed), and each length's working set (S*N profile
@@ -55,9 +58,9 @@ def workload():
     return x
 
 
-def dist_init():
+def dist_init(force: bool = False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws <= 1:
+    if ws <= 1 and not force:
         return 1, 0, 0
     import torch
     import torch.distributed as dist
@@ -190,11 +193,12 @@ def _ref_job(arg):
     return (m - l + 1) * (x.size - l + 1)
 
 
-def _config(ws):
+def _config(ws, shard="rows"):
     return {"workload": "C3: planted walk n=1,000,000 (A=4, m_act=256, seed 0), m in 64..512 step 32 "
                         "(15 lengths), K=4, l=ceil(m/2), k=ceil(m/10)",
             "n": N_SERIES, "grid": [GRID[0], GRID[-1], 32], "K": K_SNIPPETS,
-            "parallelism": f"length-sharded x{ws}" if ws > 1 else "1 GPU",
+            "parallelism": (f"segment-row sharded x{ws}" if shard == "rows" else f"length-sharded x{ws}")
+                           if ws > 1 else "1 GPU",
             "l2_flush": "not needed: per-length profile matrix 15-125 GB >> 126 MB L2"}
 
 
@@ -206,11 +210,16 @@ def main():
     ap.add_argument("--impl", default="pastila", choices=["pastila", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", default=None, help="dev only: comma-separated lengths (invalidates the metric)")
+    ap.add_argument("--shard", default="rows", choices=["rows", "lengths"],
+                    help="N>1 work split: segment rows of every length (default) or whole lengths")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="test only: create the NCCL group (and use the sharded path) even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    ws, rank, local = dist_init()
+    ws, rank, local = dist_init(args.force_dist)
+    sharded = (ws > 1 or args.force_dist) and args.shard == "rows"
     import torch
 
     import paper_2401_13680_b200 as P
@@ -226,19 +235,24 @@ def main():
     xd = torch.from_numpy(x).to(f"cuda:{local}")
     series = P.TimeSeries(x)
     parts = parallel.length_partition([P.default_cost(N_SERIES, m) for m in grid], ws)
-    mine = [grid[i] for i in parts[rank]]
+    mine = grid if sharded else [grid[i] for i in parts[rank]]
+
+    def search(s, m):
+        """one length: this rank's share (all of it at N=1), plus the Eq. 18 score"""
+        if sharded:
+            r = parallel.select_snippets_sharded(s, P.MPdistParams(m), K_SNIPPETS)
+        else:
+            r = P.select_snippets(s, P.MPdistParams(m), K_SNIPPETS)
+        return r, P.criterion_score(r)
 
     def device_step():
         # inputs resident in HBM: device-to-device reload + prefix sums, then all my lengths
         ctx.call("pst_set_series_dev", C.c_void_p(xd.data_ptr()), C.c_int64(x.size))
         ctx._series_key, ctx._series_ref = (id(series.values), series.values.ctypes.data, x.size), series.values
-        out = {}
-        for m in mine:
-            out[m] = P.select_snippets(series, P.MPdistParams(m), K_SNIPPETS)
-        return out
+        return {m: search(series, m) for m in mine}
 
     def barrier():
-        if ws > 1:
+        if ws > 1 or args.force_dist:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
@@ -264,7 +278,7 @@ def main():
     ctx.call("pst_timing", 0)
     launches = ctx.launches() - l0
     barrier()
-    if ws > 1:
+    if ws > 1 or args.force_dist:
         t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
@@ -272,25 +286,33 @@ def main():
     # ---- e2e through the public API (host buffers in, results out) ----------------------
     def e2e_step():
         s = P.TimeSeries(np.array(x))  # fresh host object -> H2D upload inside the step
+        if sharded:
+            return {m: search(s, m)[1] for m in grid}
         if ws > 1:
-            from paper_2401_13680_b200.scheduler import job_weights, run_jobs
+            from paper_2401_13680_b200.scheduler import job_weights
 
             jobs = [P.MPdistParams(m) for m in grid]
             timings = parallel.run_sharded(s, jobs, K_SNIPPETS, job_weights(s, jobs, None))
-            return {p.snippet_size: r for p, r, _ in timings}
+            return {p.snippet_size: P.criterion_score(r) for p, r, _ in timings}
         rep, results = P.select_length(s, grid, K_SNIPPETS, training_log=False)
-        return results
+        return {c.snippet_size: c.score for c in rep.candidates}
     barrier()
     t0 = time.perf_counter()
     e2e_res = e2e_step()
     e2e_s = time.perf_counter() - t0
-    if ws > 1:
+    if ws > 1 or args.force_dist:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
 
     total_pairs = sum(pairs_of(N_SERIES, m) for m in grid)
-    my_pairs = sum(pairs_of(N_SERIES, m) for m in mine)
+    if sharded:  # this rank's segment range of every length
+        my_pairs = 0
+        for m in grid:
+            lo, hi = parallel.segment_ranges(N_SERIES // m, parallel.world_size())[parallel.rank()]
+            my_pairs += pairs_of(N_SERIES, m) // (N_SERIES // m) * (hi - lo)
+    else:
+        my_pairs = sum(pairs_of(N_SERIES, m) for m in mine)
     value = total_pairs / (ms / 1e3)
     d2h = sum(K_SNIPPETS * (N_SERIES - m + 1) * 8 + (N_SERIES - m + 1) * 12 + N_SERIES * 8
               + (N_SERIES // m) * 8 for m in grid)
@@ -309,7 +331,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "seconds_per_sweep": ms / 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(ws),
+            "config": _config(ws, args.shard),
             "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "seconds": e2e_s,
                     "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "fp64", "kernel": "k_mpdist (profile tile kernel)",
@@ -319,13 +341,13 @@ def main():
                          "kernel_ms_per_step": kms.value / args.steps,
                          "kernel_share_of_step": (kms.value / args.steps) / ms},
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
-            "m_best": max(((m, r.criterion_ or 0.0) for m, r in e2e_res.items()), key=lambda t: (t[1], -t[0]))[0],
+            "m_best": max(e2e_res.items(), key=lambda t: (t[1], -t[0]))[0],
         }
         if args.grid:
             line["config"]["dev_grid_override"] = grid
             line["invalid"] = "grid override: not the metric configuration"
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if ws > 1 or args.force_dist:
         torch.distributed.destroy_process_group()
     return 0
 

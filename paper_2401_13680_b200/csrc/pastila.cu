@@ -703,7 +703,7 @@ static int run_select_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int6
 
 // Rows of D that fit the device next to the profile-kernel scratch; the
 // whole S x N matrix when it fits (PASTILA_STREAM_ROWS forces a chunk size).
-static int64_t profile_chunk_rows(pst_ctx* c, int64_t S, int64_t N) {
+static int64_t profile_chunk_rows(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
   if (const char* e = getenv("PASTILA_STREAM_ROWS")) {
     const int64_t v = atoll(e);
     if (v >= 1 && v < S) return v;
@@ -711,7 +711,10 @@ static int64_t profile_chunk_rows(pst_ctx* c, int64_t S, int64_t N) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return S;
   const size_t have = fr + c->D_bytes;  // D is reallocated in place
-  const size_t reserve = ((size_t)14 << 30) + (size_t)N * 8 * 16;  // kernel scratch (2 x 6 GB) + work buffers
+  // profile-kernel scratch: two buffers of at least one segment's AB tiles (w x Tp per tile, Tp <= 1.1 T)
+  // plus column minima, or 2 x 6 GB; work buffers; slack
+  const size_t seg_scratch = (size_t)N * 8 * (size_t)(w + w / 10 + 2);
+  const size_t reserve = std::max((size_t)12 << 30, 2 * seg_scratch) + (size_t)N * 8 * 16 + ((size_t)2 << 30);
   if (have <= reserve) return 1;
   const int64_t rows = (int64_t)((have - reserve) / ((size_t)N * 8));
   return rows >= S ? S : (rows < 1 ? 1 : rows);
@@ -734,7 +737,7 @@ int pst_profile_reduce_dev(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t 
                   (long long)S);
     return PST_EINVAL;
   }
-  int64_t chunk = profile_chunk_rows(c, seg_hi - seg_lo, N);
+  int64_t chunk = profile_chunk_rows(c, seg_hi - seg_lo, N, m - l + 1);
   PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)chunk * N * sizeof(double)));
   for (int64_t s0 = seg_lo; s0 < seg_hi; s0 += chunk) {
     const int64_t rows = std::min(chunk, seg_hi - s0);
@@ -769,7 +772,7 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
     pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
     return PST_EINVAL;
   }
-  const int64_t chunk = profile_chunk_rows(c, S, N);
+  const int64_t chunk = profile_chunk_rows(c, S, N, m - l + 1);
   if (chunk < S) return run_select_streamed(c, m, l, k, S, N, n, K, chunk, res);
   PST_TRY(pst_ensure((void**)&c->D, &c->D_bytes, (size_t)S * N * sizeof(double)));
   PST_TRY(launch_mpdist(c, m, l, k, 0, S, c->D, N));

@@ -164,13 +164,15 @@ def run_reference(args):
         return tot, time.perf_counter() - t0
     for _ in range(args.warmup):
         step()
-    vals = []
+    vals, secs = [], []
     for _ in range(args.steps):
         p, dt = step()
         vals.append(p / dt)
+        secs.append(dt)
     v = float(np.median(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(secs)),
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(ws),
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": min(cores, len(jobs)), "kind": "port",

@@ -324,6 +324,18 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         v, sample = cpu_sample_pairs_per_s(x)
         cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample}
+    issue = None
+    ip = ROOT / "profiles" / "r01_full_g256_summary.json"
+    if ip.exists() and achieved:
+        # secondary roofline: the path is bound by instruction issue (order
+        # comparisons, van Herk minima, selection counts), not by FP64 flops
+        wipp = sum(l["warp_instructions_per_pair"] for l in json.loads(ip.read_text())["launches"])
+        pps = achieved * 1e12 / FP64_FLOPS_PER_PAIR  # kernel pairs/s
+        sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+        peak_issue = 148 * 4 * sm_mhz * 1e6  # warp instructions / s (1 per scheduler per clock)
+        issue = {"warp_instr_per_pair": wipp, "achieved": pps * wipp, "peak": peak_issue,
+                 "unit": "warp-instr/s", "frac": pps * wipp / peak_issue,
+                 "source": "instructions per pair from profiles/r01_full_g256_summary.json (ncu, m=256 batch)"}
     if rank == 0:
         traffic = None
         tp = ROOT / "profiles" / "r01_traffic.json"
@@ -341,7 +353,7 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "flops_per_pair": FP64_FLOPS_PER_PAIR, "peak_source": peak_src,
                          "kernel_ms_per_step": kms.value / args.steps,
-                         "kernel_share_of_step": (kms.value / args.steps) / ms},
+                         "kernel_share_of_step": (kms.value / args.steps) / ms, "issue": issue},
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
             "m_best": max(e2e_res.items(), key=lambda t: (t[1], -t[0]))[0],
         }

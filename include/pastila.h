@@ -85,6 +85,13 @@ int pst_mpdist_profiles(pst_ctx* ctx, int64_t m, int64_t l, int64_t k,
  * all S profiles are computed on the device and never leave it; only the
  * outputs in *res are copied back.                                        */
 int pst_select_snippets(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res);
+/* select_length (length_select.py:116-182): one search per grid length, in
+ * grid order; l = ls[i] (ls NULL: ceil(m/2)), k = ceil(m/10); Eq. 18 score
+ * per length; m_best = argmax (score, -m).  indices/fracs [nm*K] in frac
+ * order, scores/areas [nm]; any output may be NULL.  Errors as the reference:
+ * "length grid is empty", "... duplicates", "... at least 2 snippets".     */
+int pst_sweep(pst_ctx* ctx, const int64_t* ms, const int64_t* ls, int64_t nm, int64_t K,
+              int64_t* indices, double* fracs, double* scores, double* areas, int64_t* m_best);
 
 /* select_snippets(..., profiles=...) on caller-supplied host profiles
  * D [S*N] of a series of length n (snippets.py:191-244).                  */

@@ -52,6 +52,7 @@ SIGNATURES = {
     "pst_areas_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "pst_colmin_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "pst_profile_reduce_dev": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "pst_sweep": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pst_criterion": (C.c_int, [_vp, _dp, _i64, _i64, C.c_double, _dp]),
     "pst_labels": (C.c_int, [_vp, _dp, _i64, _i64, _i64, _lp]),
     "pst_stream": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -779,6 +779,50 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
   return run_select(c, c->D, S, N, n, K, res);
 }
 
+// select_length (length_select.py:116-182) through the C-ABI: one search per
+// grid length in grid order (l = ls[i], or ceil(m/2) when ls is NULL; k is the
+// default ceil(m/10), length_select.py:163), Eq. 18 score per length, and
+// m_best = argmax (score, -m).  Outputs: indices/fracs [nm*K] (frac order),
+// scores/areas [nm], *m_best.
+int pst_sweep(pst_ctx* c, const int64_t* ms, const int64_t* ls, int64_t nm, int64_t K, int64_t* indices,
+              double* fracs, double* scores, double* areas, int64_t* m_best) {
+  if (!valid(c)) return PST_EINVAL;
+  if (nm < 1 || !ms) {
+    pst_set_error("length grid is empty");
+    return PST_EINVAL;
+  }
+  for (int64_t i = 0; i < nm; ++i)
+    for (int64_t j = 0; j < i; ++j)
+      if (ms[i] == ms[j]) {
+        pst_set_error("length grid has duplicates: m=%lld", (long long)ms[i]);
+        return PST_EINVAL;
+      }
+  if (K < 2) {
+    pst_set_error("length selection needs at least 2 snippets per search, got %lld", (long long)K);
+    return PST_EINVAL;
+  }
+  int64_t best = -1;
+  double best_score = 0.0;
+  for (int64_t i = 0; i < nm; ++i) {
+    const int64_t m = ms[i];
+    const int64_t l = ls ? ls[i] : (m + 1) / 2;
+    const int64_t k = (m + 9) / 10 > 1 ? (m + 9) / 10 : 1;
+    pst_snippets r;
+    memset(&r, 0, sizeof(r));
+    r.indices = indices ? indices + i * K : nullptr;
+    r.fracs = fracs ? fracs + i * K : nullptr;
+    PST_TRY(pst_select_snippets(c, m, l, k, K, &r));
+    if (scores) scores[i] = r.criterion;
+    if (areas) areas[i] = r.profile_area;
+    if (best < 0 || r.criterion > best_score || (r.criterion == best_score && m < ms[best])) {
+      best = i;
+      best_score = r.criterion;
+    }
+  }
+  if (m_best) *m_best = ms[best];
+  return PST_OK;
+}
+
 // select_snippets(..., profiles=...) (snippets.py:191-196): greedy + attribution on
 // caller-supplied host profiles D [S*N].
 int pst_select_from_profiles(pst_ctx* c, const double* Dh, int64_t S, int64_t N, int64_t n, int64_t K,

@@ -210,3 +210,35 @@ def test_errors_match_reference_wording():
         P.mpdist_profile(s, 4, P.MPdistParams(10))
     with pytest.raises(ValueError, match="window length"):
         P.compute_sliding_stats(s, 41)
+
+
+def test_c_abi_sweep_matches_select_length():
+    """pst_sweep (whole length selection through the C-ABI) == select_length."""
+    import ctypes as C
+
+    x, _ = planted_walk(6000, m_act=48, A=3, seed=11)
+    grid = [16, 24, 32, 48, 64]
+    K = 3
+    rep, results = P.select_length(P.TimeSeries(x), grid, K, training_log=False)
+    ctx = _native.context()
+    ctx.set_series(x)
+    ms = np.array(grid, dtype=np.int64)
+    idx = np.zeros(len(grid) * K, dtype=np.int64)
+    fr = np.zeros(len(grid) * K)
+    sc = np.zeros(len(grid))
+    ar = np.zeros(len(grid))
+    mb = np.zeros(1, dtype=np.int64)
+    ctx.call("pst_sweep", ms.ctypes.data_as(C.c_void_p), None, len(grid), K, idx.ctypes.data_as(C.c_void_p),
+             fr.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p), ar.ctypes.data_as(C.c_void_p),
+             mb.ctypes.data_as(C.c_void_p))
+    assert int(mb[0]) == rep.m_best
+    for i, m in enumerate(grid):
+        assert list(idx[i * K:(i + 1) * K]) == [s.index for s in results[m].snippets]
+        assert list(fr[i * K:(i + 1) * K]) == [s.frac for s in results[m].snippets]
+    assert list(sc) == [c.score for c in rep.candidates]
+    assert list(ar) == [c.profile_area for c in rep.candidates]
+    with pytest.raises(ValueError, match="duplicates"):
+        ctx.call("pst_sweep", np.array([16, 16], dtype=np.int64).ctypes.data_as(C.c_void_p), None, 2, K,
+                 None, None, None, None, None)
+    with pytest.raises(ValueError, match="at least 2"):
+        ctx.call("pst_sweep", ms.ctypes.data_as(C.c_void_p), None, len(grid), 1, None, None, None, None, None)

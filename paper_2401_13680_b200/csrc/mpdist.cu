@@ -163,22 +163,24 @@ __device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, 
   for (int b0 = warp * g.bpw; b0 < g.nblk; b0 += nw * g.bpw) {  // warp-uniform trip count
     const bool live = b0 + g.sub < g.nblk;  // lane group has a block this iteration
     const int bb = (b0 + g.sub) * w, bn = bb + w;
+    // positions past the block end read the block's last column instead of +inf:
+    // it lies in every suffix of the block, and prefix values past the end are
+    // never stored, so the minima are unchanged (groups without a block read block 0)
+    const double* Es = E + (live ? bb : 0) + g.u0;
+    const double* Ep = E + (live ? bn : w) + g.u0;
+    const int tlim = w - 1 - g.u0;
     double sf[CH], pr[CH];
     double run = PST_INF;
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t) {
-      const int u = g.u0 + t;
-      const double v = (live && u < w) ? E[bb + u] : PST_INF;
-      run = dmin(run, v);
+      run = dmin(run, Es[min(t, tlim)]);
       sf[t] = run;
     }
     double totS = run;
     run = PST_INF;
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      const int u = g.u0 + t;
-      const double v = (live && u < w) ? E[bn + u] : PST_INF;
-      run = dmin(run, v);
+      run = dmin(run, Ep[min(t, tlim)]);
       pr[t] = run;
     }
     double totP = run;
@@ -219,22 +221,21 @@ __device__ __forceinline__ void vh_rows2_reg(const double* __restrict__ E0, cons
     const bool second = tau >= g.nblk;
     const double* E = second ? E1 : E0;
     const int bb = (second ? tau - g.nblk : tau) * w, bn = bb + w;
+    const double* Es = E + (live ? bb : 0) + g.u0;  // clamped reads, as in vh_row_reg
+    const double* Ep = E + (live ? bn : w) + g.u0;
+    const int tlim = w - 1 - g.u0;
     double sf[CH], pr[CH];
     double run = PST_INF;
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t) {
-      const int u = g.u0 + t;
-      const double v = (live && u < w) ? E[bb + u] : PST_INF;
-      run = dmin(run, v);
+      run = dmin(run, Es[min(t, tlim)]);
       sf[t] = run;
     }
     double totS = run;
     run = PST_INF;
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      const int u = g.u0 + t;
-      const double v = (live && u < w) ? E[bn + u] : PST_INF;
-      run = dmin(run, v);
+      run = dmin(run, Ep[min(t, tlim)]);
       pr[t] = run;
     }
     double totP = run;

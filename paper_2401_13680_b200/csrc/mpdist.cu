@@ -1243,6 +1243,27 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
   // tile geometry: NC = NT*P columns, T = NC - w + 1 windows; aim for T >= 4w
   int nt = (4 * w > 256 * 5) ? 512 : 256;
+  if (w > 160 && w <= 288) {
+    // register van Herk, long-ish windows: pick 256 or 512 threads by (lane-group
+    // slot utilisation of the van Herk rounds, one or two rows per barrier) x (tile
+    // windows / tile columns); matches the measured winner for w = 161..257
+    double best = -1.0;
+    for (int cand : {256, 512}) {
+      int lpb = 1;
+      while (lpb < 32 && lpb * 9 < w) lpb *= 2;
+      if (lpb < 8) lpb = 8;
+      const int64_t slots = (int64_t)(cand / 32) * (32 / lpb);
+      const int64_t nb = ((int64_t)cand * 5 - w + 1) / w;
+      const int64_t used = nb >= slots ? (nb / slots) * slots : nb;
+      const int64_t tasks = 2 * used <= slots ? 2 * used : used;
+      const double util = (double)tasks / (double)(((tasks + slots - 1) / slots) * slots);
+      const double halo = (double)(used * w) / (double)(used * w + w - 1);
+      if (util * halo > best + 1e-9) {
+        best = util * halo;
+        nt = cand;
+      }
+    }
+  }
   if (const char* e = getenv("PASTILA_NT_W")) nt = (w >= atoll(e)) ? 512 : 256;  // tuning experiments
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class

@@ -97,9 +97,9 @@ struct MPArgs {
   int64_t R, Tp;     // lane-run length (odd) and AB row stride Tp = 32*R >= T
   double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
   double* ba;        // scratch: allP_BA per CTA (NCmax doubles)
-  int dbg_nostore;   // debug: skip AB stores (timing experiments only)
   int dbg_flags;     // debug (PASTILA_DBGF, timing experiments only, wrong results):
-                     //   1 = selection: skip unsettled-window solves, 2 = selection: skip count pass
+                     //   1 = selection: skip unsettled-window solves, 2 = selection: skip count pass,
+                     //   4 = selection: skip the run-start solves
 };
 
 int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,

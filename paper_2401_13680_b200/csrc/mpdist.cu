@@ -7,9 +7,16 @@
 // self-column conventions), mpdist.py:146-151 (sliding minima),
 // mpdist.py:224-231 (column minima, concatenation, k-th smallest / max).
 //
-// One CTA = one segment s x one tile of T consecutive windows j in
-// [J0, J0+T).  It sweeps the w query rows q = s*m + i; the tile needs columns
-// [J0, J0+T+w-1).  All arithmetic is IEEE binary64.
+// Two kernels per batch of segments, double-buffered over two streams:
+//  * row loop (k_mpdist / k_mpdist2 / long-window layout): one CTA = one
+//    segment s x one tile of T consecutive windows j in [J0, J0+T).  It sweeps
+//    the w query rows q = s*m + i (one or two rows per barrier); the tile
+//    needs columns [J0, J0+T+w-1).  Per row: distances, column minima, van Herk
+//    row minima, and the AB row stored to HBM in lane-run order.
+//  * selection (k_select_run): k-th smallest of every window's 2w values,
+//    lanes sweeping runs of consecutive windows with the previous answer as
+//    pivot (coalesced per-lane counts, warp-cooperative exact solves).
+// All arithmetic is IEEE binary64.
 //
 // Work is expressed in "e-space": e = 1 - rho = d^2 / (2l).  d is monotone in
 // e, so minima / order statistics are taken on e and the single sqrt is
@@ -293,53 +300,6 @@ __device__ __forceinline__ void store_ab_row(const AbStore& g, const double* __r
 #pragma unroll
   for (int c = 0; c < MAXC; ++c)
     if (c < g.cnt) d[c * NT] = s[c * (NT / 32)];
-}
-
-// van Herk, shared-memory version for large w (chunks do not fit registers).
-__device__ __forceinline__ void vh_row_smem(const double* __restrict__ E, double* __restrict__ SUF,
-                                            double* __restrict__ PRE, int NC, int NJ, int w, int warp, int lane,
-                                            int nw, double* __restrict__ srow) {
-  const int nblk = (NJ + w - 1) / w;
-  const int CH = (w + 31) / 32;
-  for (int b = warp; b < nblk; b += nw) {
-    const int bb = b * w, bn = bb + w;
-    {
-      const int endb = min(bb + w, NC);
-      const int u0 = bb + lane * CH, u1 = min(u0 + CH, endb);
-      double run = PST_INF;
-      for (int c = u1 - 1; c >= u0; --c) {
-        run = dmin(run, E[c]);
-        SUF[c] = run;
-      }
-      double tot = run;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_down_sync(FULLMASK, tot, off));
-      double carry = __shfl_down_sync(FULLMASK, tot, 1);
-      if (lane == 31) carry = PST_INF;
-      for (int c = u0; c < u1; ++c) SUF[c] = dmin(SUF[c], carry);
-    }
-    {
-      const int endn = min(bn + w, NC);
-      const int u0 = bn + lane * CH, u1 = min(u0 + CH, endn);
-      double run = PST_INF;
-      for (int c = u0; c < u1; ++c) {
-        run = dmin(run, E[c]);
-        PRE[c] = run;
-      }
-      double tot = run;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) tot = dmin(tot, __shfl_up_sync(FULLMASK, tot, off));
-      double carry = __shfl_up_sync(FULLMASK, tot, 1);
-      if (lane == 0) carry = PST_INF;
-      for (int c = u0; c < u1; ++c) PRE[c] = dmin(PRE[c], carry);
-    }
-    __syncwarp();
-    for (int u = lane; u < w && bb + u < NJ; u += 32) {
-      double v = SUF[bb + u];
-      if (u > 0) v = dmin(v, PRE[bn + u - 1]);
-      srow[bb + u] = v;
-    }
-  }
 }
 
 // ---- long windows: van Herk with every block split over several warps ----
@@ -1074,7 +1034,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
   {
     double prev = 0.0;
     for (int L = 0; L < 32; ++L) {
-      if (L * R + r0 >= NJ) break;  // warp-uniform
+      if (L * R + r0 >= NJ || (a.dbg_flags & 4)) break;  // warp-uniform
       int b1, b2;
       prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2, colbuf);
       if (lane == L) {
@@ -1337,7 +1297,6 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.R = R; a.Tp = Tp;
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
-  a.dbg_nostore = getenv("PASTILA_NOSTORE") ? 1 : 0;
   a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
   if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));

@@ -109,11 +109,47 @@ __device__ __forceinline__ double above_min(const WinVals<TM>& v, double p) {  /
 }
 
 // k-th smallest; p = pivot hint (any value >= 0).  2w > k assumed.
+// Next pivot of the exact bracketing search (heuristic only: correctness comes
+// from the counts).  dist = rank distance from the current pivot to k.  Moves
+// of 1-2 ranks take adjacent-value steps; longer moves extrapolate from the
+// local spacing (pivot minus its neighbouring value, times the ranks still to
+// go, doubled on every further one-sided step) until both brackets are known,
+// then rank interpolation, then bisection.
+__device__ __forceinline__ double next_pivot(int it, bool down, int dist, double p, double nv, double lov,
+                                             double hi, int clo, int chi, int k, bool haveLo, bool haveHi,
+                                             int& grow) {
+  double np;
+  if (dist <= 2 && it < 6) {
+    np = nv;  // adjacent value (the bracket just found)
+  } else if (haveLo && haveHi) {
+    if (it < 12) {
+      const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));
+      np = lov + (hi - lov) * (double)f;
+    } else {
+      np = 0.5 * (lov + hi);
+    }
+  } else {
+    const double step = fabs(p - nv) * (double)(dist - 1) * (double)(1 << grow);
+    grow = grow < 20 ? grow + 1 : grow;
+    np = down ? nv - step : nv + step;
+  }
+  if (haveLo) np = dmax(np, lov);
+  if (haveHi) np = dmin(np, hi);
+  if (np == p) np = nv;
+  return np;
+}
+
+__device__ unsigned long long g_selstat[64];
+__device__ int g_statflag;
+__device__ __forceinline__ void selstat(int it, int kind) {
+  if (g_statflag && (threadIdx.x & 31) == 0) atomicAdd(&g_selstat[kind * 32 + min(it, 31)], 1ull);
+}
 // lt0/le0 >= 0: the counts of p are already known (skip the first pass).
 template <int TM>
 __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int lt0 = -1, int le0 = -1) {
-  double lov = -1.0, hi = PST_INF;
-  int clo = 0, chi = 2 * w;
+  double lov = -PST_INF, hi = PST_INF;
+  int clo = 0, chi = 2 * w, grow = 0;
+  bool haveLo = false, haveHi = false;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
     if (it == 0 && lt0 >= 0) {
@@ -122,33 +158,26 @@ __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int 
     } else {
       count2<TM>(v, p, lt, le);
     }
-    if (lt < k && k <= le) return p;
-    bool down = k <= lt;
+    if (lt < k && k <= le) { selstat(it, lt0 >= 0 ? 0 : 1); return p; }
+    const bool down = k <= lt;
+    double nv;
+    int dist;
     if (down) {
-      const double b = below_max<TM>(v, p);  // #(<= b) = lt
-      if (k == lt) return b;
-      hi = b;
+      nv = below_max<TM>(v, p);  // #(<= nv) = lt
+      if (k == lt) { selstat(it, lt0 >= 0 ? 0 : 1); return nv; }
+      hi = nv;
       chi = lt;
+      haveHi = true;
+      dist = lt - k;
     } else {
-      const double u = above_min<TM>(v, p);  // smallest element > p
-      if (k == le + 1) return u;
-      lov = u;
+      nv = above_min<TM>(v, p);  // smallest element > p
+      if (k == le + 1) { selstat(it, lt0 >= 0 ? 0 : 1); return nv; }
+      lov = nv;
       clo = le;
+      haveLo = true;
+      dist = k - le - 1;
     }
-    double np;
-    if (it < 2) {
-      np = down ? hi : lov;  // adjacent-value step (rank moves of 1-2 are the common case)
-    } else if (hi < PST_INF && it < 10) {
-      const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));  // heuristic pivot only
-      np = lov + (hi - lov) * (double)f;
-    } else if (hi < PST_INF) {
-      np = 0.5 * (lov + hi);
-    } else {
-      np = lov > 0.0 ? 2.0 * lov : 1.0;
-    }
-    np = dmin(dmax(np, lov), hi);
-    if (np == p) np = hi < PST_INF ? hi : 2.0 * np + 1.0;
-    p = np;
+    p = next_pivot(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
   }
   return p;
 }
@@ -882,8 +911,9 @@ __device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p
 }
 __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, int lt0 = -1, int le0 = -1) {
   const int w = v.w;
-  double lov = -1.0, hi = PST_INF;
-  int clo = 0, chi = 2 * w;
+  double lov = -PST_INF, hi = PST_INF;
+  int clo = 0, chi = 2 * w, grow = 0;
+  bool haveLo = false, haveHi = false;
   for (int it = 0; it < 256; ++it) {
     int lt, le;
     if (it == 0 && lt0 >= 0) {
@@ -894,31 +924,24 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, in
     }
     if (lt < k && k <= le) return p;
     const bool down = k <= lt;
+    double nv;
+    int dist;
     if (down) {
-      const double b = below_maxm(v, lane, p);
-      if (k == lt) return b;
-      hi = b;
+      nv = below_maxm(v, lane, p);
+      if (k == lt) return nv;
+      hi = nv;
       chi = lt;
+      haveHi = true;
+      dist = lt - k;
     } else {
-      const double u = above_minm(v, lane, p);
-      if (k == le + 1) return u;
-      lov = u;
+      nv = above_minm(v, lane, p);
+      if (k == le + 1) return nv;
+      lov = nv;
       clo = le;
+      haveLo = true;
+      dist = k - le - 1;
     }
-    double np;
-    if (it < 2) {
-      np = down ? hi : lov;
-    } else if (hi < PST_INF && it < 10) {
-      const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));  // heuristic pivot only
-      np = lov + (hi - lov) * (double)f;
-    } else if (hi < PST_INF) {
-      np = 0.5 * (lov + hi);
-    } else {
-      np = lov > 0.0 ? 2.0 * lov : 1.0;
-    }
-    np = dmin(dmax(np, lov), hi);
-    if (np == p) np = hi < PST_INF ? hi : 2.0 * np + 1.0;
-    p = np;
+    p = next_pivot(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
   }
   return p;
 }
@@ -1298,6 +1321,14 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
   a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
+  {
+    static bool once = false;
+    if (!once && getenv("PASTILA_SELSTAT")) {
+      once = true;
+      int one = 1;
+      cudaMemcpyToSymbol(g_statflag, &one, sizeof(int));
+    }
+  }
   if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));
     a.dbg_ba = c->dbg;
@@ -1348,4 +1379,9 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   PST_CUDA(cudaEventRecord(c->ev_sel[0], c->st2));
   PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[0], 0));
   return PST_OK;
+}
+
+extern "C" int pst_debug_selstat(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_selstat, 64 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -2;
 }

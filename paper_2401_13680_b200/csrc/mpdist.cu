@@ -139,11 +139,6 @@ __device__ __forceinline__ double next_pivot(int it, bool down, int dist, double
   return np;
 }
 
-__device__ unsigned long long g_selstat[64];
-__device__ int g_statflag;
-__device__ __forceinline__ void selstat(int it, int kind) {
-  if (g_statflag && (threadIdx.x & 31) == 0) atomicAdd(&g_selstat[kind * 32 + min(it, 31)], 1ull);
-}
 // lt0/le0 >= 0: the counts of p are already known (skip the first pass).
 template <int TM>
 __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int lt0 = -1, int le0 = -1) {
@@ -158,20 +153,20 @@ __device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int 
     } else {
       count2<TM>(v, p, lt, le);
     }
-    if (lt < k && k <= le) { selstat(it, lt0 >= 0 ? 0 : 1); return p; }
+    if (lt < k && k <= le) return p;
     const bool down = k <= lt;
     double nv;
     int dist;
     if (down) {
       nv = below_max<TM>(v, p);  // #(<= nv) = lt
-      if (k == lt) { selstat(it, lt0 >= 0 ? 0 : 1); return nv; }
+      if (k == lt) return nv;
       hi = nv;
       chi = lt;
       haveHi = true;
       dist = lt - k;
     } else {
       nv = above_min<TM>(v, p);  // smallest element > p
-      if (k == le + 1) { selstat(it, lt0 >= 0 ? 0 : 1); return nv; }
+      if (k == le + 1) return nv;
       lov = nv;
       clo = le;
       haveLo = true;
@@ -1321,14 +1316,6 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
   a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
-  {
-    static bool once = false;
-    if (!once && getenv("PASTILA_SELSTAT")) {
-      once = true;
-      int one = 1;
-      cudaMemcpyToSymbol(g_statflag, &one, sizeof(int));
-    }
-  }
   if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));
     a.dbg_ba = c->dbg;
@@ -1379,9 +1366,4 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   PST_CUDA(cudaEventRecord(c->ev_sel[0], c->st2));
   PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[0], 0));
   return PST_OK;
-}
-
-extern "C" int pst_debug_selstat(unsigned long long* out) {
-  cudaDeviceSynchronize();
-  return cudaMemcpyFromSymbol(out, g_selstat, 64 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -2;
 }

@@ -1246,7 +1246,8 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class
   // columns per lane in the register van Herk (measured best on B200, tools/tune.py)
-  int chm = (w <= 24) ? 3 : (w <= 128) ? 9 : (w <= 160) ? 5 : (w <= 288) ? 9 : 0;
+  int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 56) ? 9 : (w <= 72) ? 5 : (w <= 128) ? 9 : (w <= 160) ? 5
+          : (w <= 288) ? 9 : 0;
   if (const char* e = getenv("PASTILA_CHM")) {  // tuning experiments
     const int v = atoi(e);
     if ((v == 3 || v == 5 || v == 9) && 32 * v >= w) chm = v;

@@ -1176,6 +1176,7 @@ template <int NT>
 int launch_nt2(pst_ctx* c, const MPArgs& a, dim3 grid, int chm, size_t smem) {
   if (chm == 3) return launch_p2<5, NT, 3>(c, a, grid, smem);
   if (chm == 5) return launch_p2<5, NT, 5>(c, a, grid, smem);
+  if (chm == 7) return launch_p2<5, NT, 7>(c, a, grid, smem);
   return launch_p2<5, NT, 9>(c, a, grid, smem);
 }
 
@@ -1183,6 +1184,7 @@ template <int NT>
 int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, int chm, size_t smem) {
   if (chm == 3) return P == 5 ? launch_p<5, NT, 3>(c, a, grid, smem) : launch_p<3, NT, 3>(c, a, grid, smem);
   if (chm == 5) return P == 5 ? launch_p<5, NT, 5>(c, a, grid, smem) : launch_p<3, NT, 5>(c, a, grid, smem);
+  if (chm == 7) return P == 5 ? launch_p<5, NT, 7>(c, a, grid, smem) : launch_p<3, NT, 7>(c, a, grid, smem);
   if (chm == 9) return P == 5 ? launch_p<5, NT, 9>(c, a, grid, smem) : launch_p<3, NT, 9>(c, a, grid, smem);
   switch (P) {
     case 9: return launch_p<9, NT, 0>(c, a, grid, smem);
@@ -1246,11 +1248,11 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class
   // columns per lane in the register van Herk (measured best on B200, tools/tune.py)
-  int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 56) ? 9 : (w <= 72) ? 5 : (w <= 128) ? 9 : (w <= 160) ? 5
-          : (w <= 288) ? 9 : 0;
+  int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 56) ? 7 : (w <= 72) ? 5 : (w <= 112) ? 7 : (w <= 128) ? 9
+          : (w <= 160) ? 5 : (w <= 224) ? 7 : (w <= 288) ? 9 : 0;
   if (const char* e = getenv("PASTILA_CHM")) {  // tuning experiments
     const int v = atoi(e);
-    if ((v == 3 || v == 5 || v == 9) && 32 * v >= w) chm = v;
+    if ((v == 3 || v == 5 || v == 7 || v == 9) && 32 * v >= w) chm = v;
     if (v == 0) chm = 0;  // split shared-memory van Herk
   }
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;

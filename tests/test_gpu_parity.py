@@ -97,7 +97,7 @@ def test_mpdist_random_vs_oracle(seed):
         np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
 
 
-@pytest.mark.parametrize("m", [24, 48, 80, 96, 97, 160, 161, 288, 289, 600, 1100, 2048, 4096])
+@pytest.mark.parametrize("m", [24, 48, 80, 96, 97, 128, 160, 161, 224, 400, 288, 289, 600, 1100, 2048, 4096])
 def test_mpdist_window_classes_vs_oracle(m):
     """Every register class boundary of the row / selection kernels and the
     long-window paths (w > 288 shared-memory van Herk, w > 512 gather selection)."""

@@ -242,3 +242,19 @@ def test_c_abi_sweep_matches_select_length():
                  None, None, None, None, None)
     with pytest.raises(ValueError, match="at least 2"):
         ctx.call("pst_sweep", ms.ctypes.data_as(C.c_void_p), None, len(grid), 1, None, None, None, None, None)
+
+
+@pytest.mark.parametrize("m", [64, 96, 128, 256, 288, 320, 400, 448, 512])
+def test_full_size_tiles_vs_oracle(m):
+    """n large enough that every tile is full width (T up to 2316 windows, 512-thread
+    tiles and the two-row kernel where the geometry rules pick them)."""
+    from paper_2401_13680_b200.datagen import planted_walk as pw
+
+    x, _ = pw(60000, m_act=256, A=4, seed=m)
+    params = P.MPdistParams(m)
+    st = O.sliding_stats(x, params.window_size)
+    S = x.size // m
+    for seg in (1, S // 2):
+        got = P.mpdist_profile(P.TimeSeries(x), seg, params).values
+        ref = O.mpdist_profile(x, seg, m, params.window_size, params.k, st, col_chunk=20000)
+        np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)

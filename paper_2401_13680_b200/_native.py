@@ -7,6 +7,7 @@ cause.  One context per (process, device); one process per GPU.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import threading
@@ -103,7 +104,11 @@ def ptr(a: np.ndarray | None, ctype=C.c_double):
 
 
 class Context:
-    """One device context: owns the uploaded series and device buffers."""
+    """One device context: owns the uploaded series and device buffers.
+
+    A context is shared by all threads of a process that use its GPU (ctypes
+    releases the GIL), so every upload-then-compute sequence runs under the
+    context's lock: ``with ctx.using(values): ctx.call(...)``."""
 
     def __init__(self, device: int):
         lib = load_library()
@@ -113,6 +118,14 @@ class Context:
         self.device = int(device)
         self._series_key = None
         self._series_ref = None
+        self.lock = threading.RLock()
+
+    @contextlib.contextmanager
+    def using(self, values: np.ndarray):
+        """Hold the context with ``values`` as its current series."""
+        with self.lock:
+            self.set_series(values)
+            yield self
 
     def close(self):
         if self.h:
@@ -120,6 +133,10 @@ class Context:
             self.h = None
 
     def set_series(self, values: np.ndarray) -> None:
+        with self.lock:
+            self._set_series(values)
+
+    def _set_series(self, values: np.ndarray) -> None:
         key = (id(values), values.ctypes.data, values.size)
         if key == self._series_key and self._series_ref is values:
             return
@@ -129,7 +146,8 @@ class Context:
         self._series_ref = values
 
     def call(self, name: str, *args):
-        _check(getattr(load_library(), name)(self.h, *args), name)
+        with self.lock:
+            _check(getattr(load_library(), name)(self.h, *args), name)
 
     def launches(self) -> int:
         return int(load_library().pst_launch_count(self.h))

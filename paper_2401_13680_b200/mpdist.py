@@ -136,12 +136,11 @@ def _check_profile_args(series: TimeSeries, params: MPdistParams, stats) -> None
 
 def profiles_host(series: TimeSeries, params: MPdistParams, seg_lo: int, seg_hi: int) -> np.ndarray:
     """Profiles of segments [seg_lo, seg_hi) computed on the GPU, copied to host."""
-    ctx = _native.context()
-    ctx.set_series(series.values)
     N = series.n - params.snippet_size + 1
     out = np.empty((seg_hi - seg_lo, N))
-    ctx.call("pst_mpdist_profiles", int(params.snippet_size), int(params.window_size), int(params.k),
-             int(seg_lo), int(seg_hi), _native.ptr(out))
+    with _native.context().using(series.values) as ctx:
+        ctx.call("pst_mpdist_profiles", int(params.snippet_size), int(params.window_size), int(params.k),
+                 int(seg_lo), int(seg_hi), _native.ptr(out))
     return out
 
 

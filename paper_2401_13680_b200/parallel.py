@@ -164,15 +164,15 @@ class DeviceRows:
 
         self.C = C
         self.ctx = _native.context()
-        self.ctx.set_series(series.values)
         self.dev = torch.device("cuda", self.ctx.device)
         n, m = series.n, params.snippet_size
         self.N = n - m + 1
         self.rows = seg_hi - seg_lo
         self.D = torch.empty((self.rows, self.N), dtype=torch.float64, device=self.dev)
-        self.ctx.call("pst_profiles_dev", int(m), int(params.window_size), int(params.k), int(seg_lo),
-                      int(seg_hi), C.c_void_p(self.D.data_ptr()), C.c_int64(self.N))
-        self.ctx.call("pst_sync")
+        with self.ctx.using(series.values):
+            self.ctx.call("pst_profiles_dev", int(m), int(params.window_size), int(params.k), int(seg_lo),
+                          int(seg_hi), C.c_void_p(self.D.data_ptr()), C.c_int64(self.N))
+            self.ctx.call("pst_sync")
 
     def areas(self, curve):
         import torch
@@ -222,7 +222,7 @@ class StreamedRows:
 
         self.C, self.torch = C, torch
         self.ctx = _native.context()
-        self.ctx.set_series(series.values)
+        self.values = series.values
         self.dev = torch.device("cuda", self.ctx.device)
         self.p = params
         self.lo, self.hi = seg_lo, seg_hi
@@ -251,9 +251,10 @@ class StreamedRows:
             mat = torch.zeros(self.N, dtype=torch.int32, device=self.dev)
             mxt = torch.zeros(1, dtype=torch.float64, device=self.dev)
             mv, ma, mx = (C.c_void_p(t.data_ptr()) for t in (mvt, mat, mxt))
-        self.ctx.call("pst_profile_reduce_dev", *self._mkl(), self.lo, self.hi, cptr,
-                      C.c_void_p(out.data_ptr()), mv, ma, mx)
-        self.ctx.call("pst_sync")
+        with self.ctx.using(self.values):
+            self.ctx.call("pst_profile_reduce_dev", *self._mkl(), self.lo, self.hi, cptr,
+                          C.c_void_p(out.data_ptr()), mv, ma, mx)
+            self.ctx.call("pst_sync")
         if first:
             self._colmin = (mvt.cpu().numpy(), mat.cpu().numpy().astype(np.int64) - self.lo)
             self._rowmax = float(mxt.item())
@@ -263,8 +264,10 @@ class StreamedRows:
         torch, C = self.torch, self.C
         r = torch.empty((1, self.N), dtype=torch.float64, device=self.dev)
         s = self.lo + int(i)
-        self.ctx.call("pst_profiles_dev", *self._mkl(), s, s + 1, C.c_void_p(r.data_ptr()), C.c_int64(self.N))
-        self.ctx.call("pst_sync")
+        with self.ctx.using(self.values):
+            self.ctx.call("pst_profiles_dev", *self._mkl(), s, s + 1, C.c_void_p(r.data_ptr()),
+                          C.c_int64(self.N))
+            self.ctx.call("pst_sync")
         return r[0].cpu().numpy()
 
     def colmin(self):

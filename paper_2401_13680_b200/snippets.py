@@ -121,8 +121,6 @@ def profile_area(curve) -> float:
 def _run(series: TimeSeries, params: MPdistParams, K: int, D: np.ndarray | None) -> SnippetResult:
     n, m = series.n, params.snippet_size
     S, N = n // m, n - m + 1
-    ctx = _native.context()
-    ctx.set_series(series.values)
     idx = np.empty(K, dtype=np.int64)
     fracs = np.empty(K)
     curve = np.empty(N)
@@ -134,12 +132,13 @@ def _run(series: TimeSeries, params: MPdistParams, K: int, D: np.ndarray | None)
         _native.ptr(idx, _native.C.c_int64), _native.ptr(fracs), _native.ptr(curve), _native.ptr(prof),
         _native.ptr(counts, _native.C.c_int64), _native.ptr(nearest, _native.C.c_int32),
         _native.ptr(labels, _native.C.c_int64), 0.0, 0.0, 0.0, 0)
-    if D is None:
-        ctx.call("pst_select_snippets", int(m), int(params.window_size), int(params.k), int(K),
-                 _native.C.byref(out))
-    else:
-        ctx.call("pst_select_from_profiles", _native.ptr(D), int(S), int(N), int(n), int(K),
-                 _native.C.byref(out))
+    with _native.context().using(series.values) as ctx:
+        if D is None:
+            ctx.call("pst_select_snippets", int(m), int(params.window_size), int(params.k), int(K),
+                     _native.C.byref(out))
+        else:
+            ctx.call("pst_select_from_profiles", _native.ptr(D), int(S), int(N), int(n), int(K),
+                     _native.C.byref(out))
     snippets = tuple(
         Snippet(index=int(i), start=int(i) * m, length=m, frac=float(f),
                 neighbors=np.flatnonzero(nearest == i).astype(np.int64))

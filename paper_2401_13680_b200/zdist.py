@@ -51,10 +51,9 @@ def _check_stats(stats: SlidingStats, l: int) -> None:
 
 
 def _rows(series: TimeSeries, l: int, q0: int, rows: int, method: int) -> np.ndarray:
-    ctx = _native.context()
-    ctx.set_series(series.values)
     out = np.empty((rows, series.n - l + 1))
-    ctx.call("pst_distance_rows", int(l), int(q0), int(rows), int(method), _native.ptr(out))
+    with _native.context().using(series.values) as ctx:
+        ctx.call("pst_distance_rows", int(l), int(q0), int(rows), int(method), _native.ptr(out))
     return out
 
 

@@ -75,3 +75,30 @@ def test_sharded_api_device_backends(series, monkeypatch, backend):
         dist.destroy_process_group()
     _same(resident, got)
     assert got.profile_area == pytest.approx(resident.profile_area, rel=1e-12)
+
+
+def test_threads_share_a_context():
+    """Two threads, two series, one device context: results equal the sequential ones
+    (every upload-then-compute sequence holds the context lock)."""
+    import threading
+
+    xa, _ = planted_walk(12000, m_act=60, A=3, seed=21)
+    xb, _ = planted_walk(12000, m_act=80, A=2, seed=22)
+    p = P.MPdistParams(60)
+    ref = {k: [s.index for s in P.select_snippets(P.TimeSeries(x), p, 3).snippets] for k, x in (("a", xa), ("b", xb))}
+    got, errs = {"a": [], "b": []}, []
+
+    def work(key, x):
+        try:
+            for _ in range(4):
+                got[key].append([s.index for s in P.select_snippets(P.TimeSeries(x), p, 3).snippets])
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=("a", xa)), threading.Thread(target=work, args=("b", xb))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    assert all(g == ref["a"] for g in got["a"]) and all(g == ref["b"] for g in got["b"])

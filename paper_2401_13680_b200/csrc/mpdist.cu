@@ -1137,6 +1137,12 @@ int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
 // so the warp-cooperative run starts are amortized.
 template <int TM>
 int launch_sel_tm(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
+  if (const char* e = getenv("PASTILA_NWS")) {  // tuning experiments
+    const int v = atoi(e);
+    if (v == 1) return launch_sel_w<1, TM>(c, a, grid, NCmax);
+    if (v == 2) return launch_sel_w<2, TM>(c, a, grid, NCmax);
+    if (v == 4) return launch_sel_w<4, TM>(c, a, grid, NCmax);
+  }
   if (a.R >= 48) return launch_sel_w<4, TM>(c, a, grid, NCmax);
   if (a.R >= 24) return launch_sel_w<2, TM>(c, a, grid, NCmax);
   return launch_sel_w<1, TM>(c, a, grid, NCmax);

@@ -52,7 +52,9 @@ typedef struct pst_snippets {
   int64_t unassigned;      /* out: windows whose nearest is not chosen    */
 } pst_snippets;
 
-/* ---- context --------------------------------------------------------- */
+/* ---- context (no reference counterpart: the reference is host-only; one
+ * context per process and GPU owns the uploaded series and device buffers;
+ * pst_last_error is per thread and carries the reference's ValueError text) */
 int pst_create(int device, pst_ctx** out);
 int pst_destroy(pst_ctx* ctx);
 const char* pst_last_error(void);
@@ -105,16 +107,19 @@ int pst_criterion(pst_ctx* ctx, const double* P, int64_t K, int64_t N, double pr
 int pst_labels(pst_ctx* ctx, const double* P, int64_t K, int64_t N, int64_t n, int64_t* labels);
 
 /* ---- device-level API (multi-GPU sharding / benchmark) ----------------
- * Profiles of segments [seg_lo, seg_hi) written to a caller-owned device
- * matrix D_dev (row stride ld >= n-m+1).                                   */
+ * segment_profiles (snippets.py:119-128, mpdist.py:179-232) for segments
+ * [seg_lo, seg_hi), written to a caller-owned device matrix D_dev (row
+ * stride ld >= n-m+1).                                                     */
 int pst_profiles_dev(pst_ctx* ctx, int64_t m, int64_t l, int64_t k,
                      int64_t seg_lo, int64_t seg_hi, double* D_dev, int64_t ld);
 /* Greedy-step areas sum_j min(D[s][j], curve[j]) for rows of D_dev
- * (curve_dev == NULL means +inf, i.e. plain row sums).  areas_dev [rows].  */
+ * (snippets.py:201-206; curve_dev == NULL means +inf, i.e. plain row sums).
+ * areas_dev [rows].                                                        */
 int pst_areas_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
                   const double* curve_dev, double* areas_dev);
-/* Per-window minimum value and first argmin over rows (ties -> lower row),
- * row indices offset by row_base.  minval_dev [N], argmin_dev [N].        */
+/* Per-window minimum value and first argmin over rows (snippets.py:212,
+ * ties -> lower row), row indices offset by row_base.  minval_dev [N],
+ * argmin_dev [N].                                                          */
 int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
                    int64_t row_base, double* minval_dev, int32_t* argmin_dev);
 /* Profiles of segments [seg_lo, seg_hi) computed in device-sized chunks and

@@ -58,6 +58,12 @@ def workload():
     return x
 
 
+def torch_dist_backend():
+    import torch.distributed as dist
+
+    return dist.get_backend() if dist.is_initialized() else None
+
+
 def dist_init(force: bool = False):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws <= 1 and not force:
@@ -66,10 +72,17 @@ def dist_init(force: bool = False):
     import torch.distributed as dist
 
     lr = int(os.environ.get("LOCAL_RANK", "0"))
-    os.environ["PASTILA_DEVICE"] = str(lr)
-    torch.cuda.set_device(lr)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
-    return ws, dist.get_rank(), lr
+    # test only: PASTILA_FORCE_DEVICE / PASTILA_DIST_BACKEND=gloo run the N>1 code path
+    # with several ranks on one GPU (host-side collectives, no cross-rank kernel waits)
+    dev = int(os.environ.get("PASTILA_FORCE_DEVICE", lr))
+    os.environ["PASTILA_DEVICE"] = str(dev)
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("PASTILA_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group(backend)
+    return ws, dist.get_rank(), dev
 
 
 class ClockSampler:
@@ -222,6 +235,8 @@ def main():
 
     ws, rank, local = dist_init(args.force_dist)
     sharded = (ws > 1 or args.force_dist) and args.shard == "rows"
+    dist_on = ws > 1 or args.force_dist
+    red_dev = (f"cuda:{local}" if not dist_on or torch_dist_backend() == "nccl" else "cpu")
     import torch
 
     import paper_2401_13680_b200 as P
@@ -281,7 +296,7 @@ def main():
     launches = ctx.launches() - l0
     barrier()
     if ws > 1 or args.force_dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
 
@@ -303,7 +318,7 @@ def main():
     e2e_res = e2e_step()
     e2e_s = time.perf_counter() - t0
     if ws > 1 or args.force_dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
 

@@ -102,3 +102,53 @@ def test_threads_share_a_context():
         t.join()
     assert not errs
     assert all(g == ref["a"] for g in got["a"]) and all(g == ref["b"] for g in got["b"])
+
+
+def _two_rank_worker(rank, port, backend_name, out):
+    """one of two gloo ranks sharing cuda:0 (host-side collectives only)"""
+    import torch.distributed as dist
+
+    os.environ["PASTILA_DEVICE"] = "0"
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+    import paper_2401_13680_b200 as PP
+    from paper_2401_13680_b200 import parallel as par
+    from paper_2401_13680_b200.datagen import planted_walk as pw
+
+    x, _ = pw(20000, m_act=120, A=3, seed=0)
+    s, p = PP.TimeSeries(x), PP.MPdistParams(120)
+    lo, hi = par.segment_ranges(x.size // 120, 2)[rank]
+    if backend_name == "StreamedRows":
+        os.environ["PASTILA_STREAM_ROWS"] = "9"
+    b = getattr(par, backend_name)(s, p, lo, hi)
+    r = par.select_snippets_sharded(s, p, 3, backend=b)
+    if rank == 0:
+        out.put(([q.index for q in r.snippets], [q.frac for q in r.snippets], r.curve,
+                 np.vstack([q.values for q in r.profiles]), r.profile_max, r.segment_window_counts))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("backend", ["DeviceRows", "StreamedRows"])
+def test_two_ranks_row_sharded_on_device(series, backend):
+    """segment-row sharding with device backends across two processes (gloo, one GPU)
+    == the single-process resident result"""
+    import torch.multiprocessing as mp
+
+    ref = P.select_snippets(P.TimeSeries(series), P.MPdistParams(120), 3)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, port, backend, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    idx, fr, curve, prof, pmax, counts = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert idx == [s_.index for s_ in ref.snippets] and fr == [s_.frac for s_ in ref.snippets]
+    np.testing.assert_array_equal(curve, ref.curve)
+    np.testing.assert_array_equal(prof, np.vstack([p_.values for p_ in ref.profiles]))
+    assert pmax == ref.profile_max
+    np.testing.assert_array_equal(counts, ref.segment_window_counts)

@@ -258,3 +258,33 @@ def test_full_size_tiles_vs_oracle(m):
         got = P.mpdist_profile(P.TimeSeries(x), seg, params).values
         ref = O.mpdist_profile(x, seg, m, params.window_size, params.k, st, col_chunk=20000)
         np.testing.assert_allclose(got, ref, atol=1e-6, rtol=1e-6)
+
+
+class TestReferenceEdgeCases:
+    """The reference's own degenerate cases (test_length_select.py:100-135,
+    test_snippets.py:84-100) on the GPU path."""
+
+    def test_constant_series_ties_to_smallest(self):
+        report, _ = P.select_length(P.TimeSeries(np.full(256, 3.5)), [8, 16, 32], 2, training_log=False)
+        assert all(c.score == 0.0 for c in report.candidates)
+        assert report.m_best == 8
+
+    def test_homogeneous_series_single_snippet(self):
+        x = np.tile([0.0, 2.0, 1.0, 3.0, 2.0, 0.0, 1.0, 2.0], 8)
+        r = P.select_snippets(P.TimeSeries(x), P.MPdistParams(8), 1)
+        assert len(r.snippets) == 1 and r.snippets[0].frac == 1.0 and r.snippets[0].index == 0
+
+    def test_scale_invariance_and_grid_order(self):
+        v, _ = two_regime_series(n=512, period=16, block_len=64, noise=0.05, seed=6)
+        base, _ = P.select_length(P.TimeSeries(v), [8, 16, 32], 2, training_log=False)
+        scaled, _ = P.select_length(P.TimeSeries(v * 3.7), [8, 16, 32], 2, training_log=False)
+        assert scaled.m_best == base.m_best
+        for a, b in zip(base.candidates, scaled.candidates):
+            assert a.score == pytest.approx(b.score, rel=1e-6)
+        rep, _ = P.select_length(P.TimeSeries(v), [32, 8, 16], 2, training_log=False)
+        assert [c.snippet_size for c in rep.candidates] == [32, 8, 16]
+
+    def test_singleton_grid(self):
+        v, _ = two_regime_series(n=512, period=16, block_len=64, noise=0.05, seed=5)
+        report, results = P.select_length(P.TimeSeries(v), [16], 2, training_log=False)
+        assert report.m_best == 16 and list(results) == [16]

@@ -288,3 +288,45 @@ class TestReferenceEdgeCases:
         v, _ = two_regime_series(n=512, period=16, block_len=64, noise=0.05, seed=5)
         report, results = P.select_length(P.TimeSeries(v), [16], 2, training_log=False)
         assert report.m_best == 16 and list(results) == [16]
+
+
+class TestReferenceKnownAnswers:
+    """Known-answer tests of the reference (test_zdist.py:70-95, test_mpdist.py:160-175,
+    test_labeling.py:60-80) through the GPU kernels."""
+
+    @staticmethod
+    def _row(values, seg_start, offset, l, method="sliding"):
+        s = P.TimeSeries(np.asarray(values, dtype=np.float64))
+        return P.distance_row(s, P.compute_sliding_stats(s, l), seg_start, offset, l, method=method)
+
+    def test_self_column_is_exact_zero(self):
+        v = np.random.default_rng(0).standard_normal(40)
+        assert self._row(v, 8, 3, 5).entries[11] == 0.0
+
+    def test_affine_window_matches(self):
+        row = self._row([0.0, 1.0, 2.0, 9.0, 5.0, 7.0, 9.0, 1.0], 0, 0, 3)
+        assert row.entries[4] == pytest.approx(0.0, abs=1e-7)
+
+    def test_spec_value_reversed_window(self):
+        row = self._row([1.0, 2.0, 3.0, 3.0, 2.0, 1.0], 0, 0, 3)
+        assert row.entries[3] == pytest.approx(2 * np.sqrt(3), abs=1e-9)
+
+    def test_methods_agree(self):
+        v = np.random.default_rng(3).standard_normal(200)
+        np.testing.assert_allclose(self._row(v, 20, 4, 16).entries,
+                                   self._row(v, 20, 4, 16, method="direct").entries, atol=1e-9)
+
+    def test_antiphase_example(self):
+        s = P.TimeSeries([0.0, 1.0, 0.0, 1.0, 1.0, 0.0, 1.0, 0.0])
+        prof = P.mpdist_profile(s, 0, P.MPdistParams(4, window_size=2, k=1))
+        assert prof.values[4] == pytest.approx(0.0, abs=1e-9)
+
+    def test_label_boundaries_within_a_window(self):
+        v, regime = two_regime_series(n=512, period=16, block_len=128, noise=0.0, seed=2)
+        res = P.select_snippets(P.TimeSeries(v), P.MPdistParams(16), 2)
+        labels = P.label_series(res).labels
+        changes = np.flatnonzero(np.diff(labels)) + 1
+        flips = np.flatnonzero(np.diff(regime)) + 1
+        assert changes.size == flips.size and np.all(np.abs(changes - flips) < 16)
+        last = v.size - 16
+        assert np.all(labels[last:] == labels[last])

@@ -132,6 +132,24 @@ int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, i
 int pst_profile_reduce_dev(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
                            const double* curve_dev, double* areas_dev, double* minval_dev,
                            int32_t* argmin_dev, double* rowmax_dev);
+/* ---- key path evidence (no reference counterpart; the reference computes
+ * every profile value in fp64, mpdist.py:179-232) -------------------------
+ * Profile keys of segments [seg_lo, seg_hi): the high 32-bit word of the e
+ * value (e = d^2/2l) of each window's k-th smallest P_ABBA element, as the
+ * fast pass stores them; the exact profile value lies in
+ * [f(key:00000000), f(key:ffffffff)], f(e) = sqrt(2l * e).  out: host
+ * [(seg_hi-seg_lo) * (n-m+1)].                                             */
+int pst_profile_keys(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                     int32_t* out);
+/* Exact MPdist profile values D[seg[i]][win[i]] (mpdist.py:179-232 at one
+ * window), bit-identical to pst_mpdist_profiles; host arrays of cnt.      */
+int pst_window_exact(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, const int64_t* seg, const int64_t* win,
+                     int64_t cnt, double* out);
+/* Certification counters of key-path selections since the last reset:
+ * [lengths, greedy candidates evaluated exactly, greedy steps with >1
+ * candidate, uncertain attribution windows, exact window evaluations,
+ * profile_max candidates, fallbacks to the exact path, windows].         */
+int pst_cert_stats(pst_ctx* ctx, int64_t* out8, int reset);
 /* The context's CUDA stream (cudaStream_t) for caller-side event timing.  */
 int pst_stream(pst_ctx* ctx, void** stream_out);
 /* Profile-kernel timing: pst_timing(ctx,1) enables + resets; pst_timing_read

@@ -56,6 +56,9 @@ SIGNATURES = {
     "pst_sweep": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pst_criterion": (C.c_int, [_vp, _dp, _i64, _i64, C.c_double, _dp]),
     "pst_labels": (C.c_int, [_vp, _dp, _i64, _i64, _i64, _lp]),
+    "pst_profile_keys": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _ip]),
+    "pst_window_exact": (C.c_int, [_vp, _i64, _i64, _i64, _lp, _lp, _i64, _dp]),
+    "pst_cert_stats": (C.c_int, [_vp, _lp, C.c_int]),
     "pst_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "pst_timing": (C.c_int, [_vp, C.c_int]),
     "pst_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

@@ -68,6 +68,16 @@ struct pst_ctx {
   // profile matrix D (S x N) + greedy buffers
   double* D = nullptr;
   size_t D_bytes = 0;
+  // key path: S x N profile keys, exact rows of greedy candidates, certification lists
+  int* Dk = nullptr;
+  size_t Dk_bytes = 0;
+  void* cert = nullptr;
+  size_t cert_bytes = 0;
+  // certification counters of the last key-path selections (pst_cert_stats):
+  // [0] lengths, [1] greedy candidates evaluated exactly, [2] greedy steps with >1
+  // candidate, [3] uncertain attribution windows, [4] exact (segment, window)
+  // evaluations, [5] max candidates, [6] fallbacks to the exact path, [7] windows
+  int64_t cert_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   void* work = nullptr;
   size_t work_bytes = 0;
   int64_t launches = 0;
@@ -86,21 +96,42 @@ struct pst_ctx {
 int pst_ensure(void** p, size_t* cap, size_t bytes);
 int pst_ensure_len(pst_ctx* c, int64_t l);
 
-// kernels launched from several translation units
+// kernels launched from several translation units.  The profile kernels are
+// templated on the value type V of their minima / order statistics: double
+// (exact e values) or int (32-bit key = high word of e, see mpdist.cu).
 struct MPArgs {
   const double *x, *mu /* centering means (LenData::mc) */, *nrm, *bias, *cbias, *df, *dg;
   int64_t n, l, m, w, k, Nl, N, T;
   int64_t seg0;      // segment of blockIdx.y == 0
-  double* D;         // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y)
+  void* D;           // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y): double d / int key
   int64_t ldD, rowD0;
-  double* ab;        // scratch, w*Tp doubles per CTA, lane-run order (see mpdist.cu)
+  void* ab;          // scratch, w*Tp values V per CTA, lane-run order (see mpdist.cu)
   int64_t R, Tp;     // lane-run length (odd) and AB row stride Tp = 32*R >= T
-  double* dbg_ba;    // optional: allP_BA of CTA (0,0) (debug)
-  double* ba;        // scratch: allP_BA per CTA (NCmax doubles)
+  void* dbg_ba;      // optional: allP_BA of CTA (0,0) (debug)
+  void* ba;          // scratch: allP_BA per CTA (NCmax values V)
   int dbg_flags;     // debug (PASTILA_DBGF, timing experiments only, wrong results):
                      //   1 = selection: skip unsettled-window solves, 2 = selection: skip count pass,
                      //   4 = selection: skip the run-start solves
 };
 
+// Tile geometry of the profile kernels for one (m, l) on one series length:
+// shared by the exact (double) and key (int) paths and by the exact
+// single-window evaluator, so that all three compute bit-identical e values.
+struct TileGeom {
+  int64_t w, N, NCmax, T, ntile, R, Tp;
+  int nt, P, chm;
+  bool rows2;
+  size_t smem_d;   // dynamic smem of the one-row kernel with V = double (geometry decisions)
+};
+int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& g);
+
 int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
                   double* D_dev, int64_t ld);
+// key path: Dk rows receive the 32-bit key (high word of e) of the k-th smallest
+// P_ABBA element instead of the distance (exact d lies in [f(lo(key)), f(hi(key))]).
+int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                       int* Dk_dev, int64_t ld);
+// exact profile values at single (segment, window) pairs, bit-identical to the
+// full profile kernels: out[i] = D[seg[i]][win[i]] (device arrays, cnt entries).
+int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* seg_dev,
+                        const int64_t* win_dev, int64_t cnt, double* out_dev);

@@ -1,7 +1,7 @@
 // MPdist profile tile kernel (north_star items 2+3): z-normalized distance
 // rows by the centered diagonal recurrence, column minima (allP_BA), row
 // sliding minima (allP_AB, van Herk / Gil-Werman blocks of width w), and the
-// exact k-th smallest of the 2w-element P_ABBA multiset of every window.
+// k-th smallest of the 2w-element P_ABBA multiset of every window.
 //
 // Reference semantics: zdist.py:74-123 (distances, constant-window and
 // self-column conventions), mpdist.py:146-151 (sliding minima),
@@ -16,7 +16,7 @@
 //  * selection (k_select_run): k-th smallest of every window's 2w values,
 //    lanes sweeping runs of consecutive windows with the previous answer as
 //    pivot (coalesced per-lane counts, warp-cooperative exact solves).
-// All arithmetic is IEEE binary64.
+// The distance arithmetic is IEEE binary64.
 //
 // Work is expressed in "e-space": e = 1 - rho = d^2 / (2l).  d is monotone in
 // e, so minima / order statistics are taken on e and the single sqrt is
@@ -26,8 +26,24 @@
 //   e(q,c)     = bias[c] - cov*nrm[q]*nrm[c]         (non-constant query)
 //              = cbias[c]                            (constant query)
 //              = 0                                   (c == q, self column)
+//
+// Value type V of the minima and the order statistic (template parameter):
+//  * double: the exact path -- profiles are d = sqrt(2l * e_k);
+//  * int:    the key path -- every e is replaced by its 32-bit key, the high
+//    word of its IEEE bit pattern read as a signed int.  For e >= +0 the key
+//    is monotone non-decreasing in e; negative e (rounding residue of an exact
+//    match, mapped to d = 0 anyway) get negative keys, below every e >= 0.
+//    Minima commute with a monotone map, so every column minimum, sliding
+//    minimum and the k-th smallest key are exactly key(exact value): the key
+//    path returns key(e_k) of the exact path's e_k, i.e. e_k lies in the
+//    2^-20-relative bucket [lo(key), hi(key)].  Same tiles, same fma order,
+//    bit-identical e values; half the shared-memory / scratch bytes, and every
+//    compare-and-select is one integer instruction instead of DSETP + 2 FSEL.
+//    pastila.cu certifies every downstream decision from these buckets and
+//    resolves the uncertain ones with exact values (k_window_exact below).
 #include "common.cuh"
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -35,9 +51,34 @@
 namespace {
 
 // NaN-free min/max (values are finite or +inf): 1 DSETP + 2 FSEL instead of the
-// ~8-instruction IEEE fmin/fmax sequence.
-__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
-__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+// ~8-instruction IEEE fmin/fmax sequence; ints: one VIMNMX.
+__device__ __forceinline__ double vmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double vmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ int vmin(int a, int b) { return min(a, b); }
+__device__ __forceinline__ int vmax(int a, int b) { return max(a, b); }
+
+template <class V>
+struct VT;
+template <>
+struct VT<double> {
+  static __device__ __forceinline__ double inf() { return PST_INF; }
+  static __device__ __forceinline__ double ninf() { return -PST_INF; }
+  static __device__ __forceinline__ double of(double e) { return e; }
+  static __device__ __forceinline__ double from_d(double v) { return v; }
+  static __device__ __forceinline__ double quarter(double v) { return v * 0.25; }
+};
+template <>
+struct VT<int> {
+  static __device__ __forceinline__ int inf() { return INT_MAX; }
+  static __device__ __forceinline__ int ninf() { return INT_MIN; }
+  static __device__ __forceinline__ int of(double e) { return __double2hiint(e); }
+  static __device__ __forceinline__ int from_d(double v) {  // key-space pivot arithmetic
+    if (!(v > -2147483648.0)) return INT_MIN;
+    if (v >= 2147483647.0) return INT_MAX;
+    return (int)floor(v);
+  }
+  static __device__ __forceinline__ int quarter(int v) { return v - (2 << 20); }  // e/4: exponent - 2
+};
 
 // ---------------------------------------------------------------- selection
 // Exact k-th smallest (1-based) of the 2w-element P_ABBA multiset of one
@@ -47,7 +88,7 @@ __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : 
 //
 // exact warp max / min of doubles via two 32-bit REDUX steps on the
 // order-preserving 64-bit key (sign-flipped bit pattern): tiny negative
-// rounding residues of e = 1 - rho order correctly.
+// rounding residues of e = 1 - rho order correctly.  Keys: one REDUX.
 __device__ __forceinline__ unsigned long long okey(double v) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(v);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
@@ -70,14 +111,16 @@ __device__ __forceinline__ double warp_min(double v) {
   const unsigned l = __reduce_min_sync(FULLMASK, kh == h ? kl : 0xffffffffu);
   return ukey(((unsigned long long)h << 32) | l);
 }
+__device__ __forceinline__ int warp_max(int v) { return __reduce_max_sync(FULLMASK, v); }
+__device__ __forceinline__ int warp_min(int v) { return __reduce_min_sync(FULLMASK, v); }
 
-template <int TM>
+template <int TM, class V>
 struct WinVals {
-  double a[TM], b[TM];
+  V a[TM], b[TM];
 };
 
-template <int TM>
-__device__ __forceinline__ void count2(const WinVals<TM>& v, double p, int& lt, int& le) {
+template <int TM, class V>
+__device__ __forceinline__ void count2(const WinVals<TM, V>& v, V p, int& lt, int& le) {
   int l1 = 0, l2 = 0;
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
@@ -87,92 +130,96 @@ __device__ __forceinline__ void count2(const WinVals<TM>& v, double p, int& lt, 
   lt = __reduce_add_sync(FULLMASK, l1);
   le = __reduce_add_sync(FULLMASK, l2);
 }
-template <int TM>
-__device__ __forceinline__ double below_max(const WinVals<TM>& v, double p) {  // largest element < p (or -inf)
-  double m = -PST_INF;
+template <int TM, class V>
+__device__ __forceinline__ V below_max(const WinVals<TM, V>& v, V p) {  // largest element < p (or -inf)
+  V m = VT<V>::ninf();
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
-    m = dmax(m, v.a[t] < p ? v.a[t] : -PST_INF);
-    m = dmax(m, v.b[t] < p ? v.b[t] : -PST_INF);
+    m = vmax(m, v.a[t] < p ? v.a[t] : VT<V>::ninf());
+    m = vmax(m, v.b[t] < p ? v.b[t] : VT<V>::ninf());
   }
   return warp_max(m);
 }
-template <int TM>
-__device__ __forceinline__ double above_min(const WinVals<TM>& v, double p) {  // smallest element > p (or +inf)
-  double m = PST_INF;
+template <int TM, class V>
+__device__ __forceinline__ V above_min(const WinVals<TM, V>& v, V p) {  // smallest element > p (or +inf)
+  V m = VT<V>::inf();
 #pragma unroll
   for (int t = 0; t < TM; ++t) {
-    m = dmin(m, v.a[t] > p ? v.a[t] : PST_INF);
-    m = dmin(m, v.b[t] > p ? v.b[t] : PST_INF);
+    m = vmin(m, v.a[t] > p ? v.a[t] : VT<V>::inf());
+    m = vmin(m, v.b[t] > p ? v.b[t] : VT<V>::inf());
   }
   return warp_min(m);
 }
 
-// k-th smallest; p = pivot hint (any value >= 0).  2w > k assumed.
 // Next pivot of the exact bracketing search (heuristic only: correctness comes
 // from the counts).  dist = rank distance from the current pivot to k.  Moves
 // of 1-2 ranks take adjacent-value steps; longer moves extrapolate from the
 // local spacing (pivot minus its neighbouring value, times the ranks still to
 // go, doubled on every further one-sided step) until both brackets are known,
-// then rank interpolation, then bisection.
-__device__ __forceinline__ double next_pivot(int it, bool down, int dist, double p, double nv, double lov,
-                                             double hi, int clo, int chi, int k, bool haveLo, bool haveHi,
-                                             int& grow) {
+// then rank interpolation, then bisection.  Keys: the same arithmetic in key
+// units (log-linear in e).
+template <class V>
+__device__ __forceinline__ V next_pivot(int it, bool down, int dist, V p, V nv, V lov, V hi, int clo, int chi,
+                                        int k, bool haveLo, bool haveHi, int& grow) {
   double np;
+  const double dp = (double)p, dnv = (double)nv, dlo = (double)lov, dhi = (double)hi;
   if (dist <= 2 && it < 6) {
-    np = nv;  // adjacent value (the bracket just found)
+    np = dnv;  // adjacent value (the bracket just found)
   } else if (haveLo && haveHi) {
     if (it < 12) {
       const float f = __fdividef((float)(k - clo) - 0.5f, (float)(chi - clo));
-      np = lov + (hi - lov) * (double)f;
+      np = dlo + (dhi - dlo) * (double)f;
     } else {
-      np = 0.5 * (lov + hi);
+      np = 0.5 * (dlo + dhi);
     }
   } else {
-    const double step = fabs(p - nv) * (double)(dist - 1) * (double)(1 << grow);
+    const double step = fabs(dp - dnv) * (double)(dist - 1) * (double)(1 << grow);
     grow = grow < 20 ? grow + 1 : grow;
-    np = down ? nv - step : nv + step;
+    np = down ? dnv - step : dnv + step;
   }
-  if (haveLo) np = dmax(np, lov);
-  if (haveHi) np = dmin(np, hi);
-  if (np == p) np = nv;
-  return np;
+  V r = VT<V>::from_d(np);
+  if (haveLo) r = vmax(r, lov);
+  if (haveHi) r = vmin(r, hi);
+  if (r == p) r = nv;
+  return r;
 }
 
 // lt0/le0 >= 0: the counts of p are already known (skip the first pass).
-template <int TM>
-__device__ double warp_select(const WinVals<TM>& v, int w, int k, double p, int lt0 = -1, int le0 = -1) {
-  double lov = -PST_INF, hi = PST_INF;
+// Every iteration removes at least one element from the bracket [lov, hi]
+// (both ends are elements), so 2w + 2 iterations always reach the answer.
+template <int TM, class V>
+__device__ V warp_select(const WinVals<TM, V>& v, int w, int k, V p, int lt0 = -1, int le0 = -1) {
+  V lov = VT<V>::ninf(), hi = VT<V>::inf();
   int clo = 0, chi = 2 * w, grow = 0;
   bool haveLo = false, haveHi = false;
-  for (int it = 0; it < 256; ++it) {
+  for (int it = 0; it < 2 * w + 2; ++it) {
     int lt, le;
     if (it == 0 && lt0 >= 0) {
       lt = lt0;
       le = le0;
     } else {
-      count2<TM>(v, p, lt, le);
+      count2<TM, V>(v, p, lt, le);
     }
     if (lt < k && k <= le) return p;
     const bool down = k <= lt;
-    double nv;
+    V nv;
     int dist;
     if (down) {
-      nv = below_max<TM>(v, p);  // #(<= nv) = lt
+      nv = below_max<TM, V>(v, p);  // #(<= nv) = lt
       if (k == lt) return nv;
       hi = nv;
       chi = lt;
       haveHi = true;
       dist = lt - k;
     } else {
-      nv = above_min<TM>(v, p);  // smallest element > p
+      nv = above_min<TM, V>(v, p);  // smallest element > p
       if (k == le + 1) return nv;
       lov = nv;
       clo = le;
       haveLo = true;
       dist = k - le - 1;
     }
-    p = next_pivot(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
+    p = next_pivot<V>(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
   }
   return p;
 }
@@ -188,53 +235,53 @@ struct VHGeom {
 };
 
 // E holds +inf beyond the tile's last column (rows never read past NC + w).
-template <int CH>
-__device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, const VHGeom& g, int warp,
-                                           int nw, double* __restrict__ srow) {
+template <int CH, class V>
+__device__ __forceinline__ void vh_row_reg(const V* __restrict__ E, int w, const VHGeom& g, int warp, int nw,
+                                           V* __restrict__ srow) {
   for (int b0 = warp * g.bpw; b0 < g.nblk; b0 += nw * g.bpw) {  // warp-uniform trip count
     const bool live = b0 + g.sub < g.nblk;  // lane group has a block this iteration
     const int bb = (b0 + g.sub) * w, bn = bb + w;
     // positions past the block end read the block's last column instead of +inf:
     // it lies in every suffix of the block, and prefix values past the end are
     // never stored, so the minima are unchanged (groups without a block read block 0)
-    const double* Es = E + (live ? bb : 0) + g.u0;
-    const double* Ep = E + (live ? bn : w) + g.u0;
+    const V* Es = E + (live ? bb : 0) + g.u0;
+    const V* Ep = E + (live ? bn : w) + g.u0;
     const int tlim = w - 1 - g.u0;
-    double sf[CH], pr[CH];
-    double run = PST_INF;
+    V sf[CH], pr[CH];
+    V run = VT<V>::inf();
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t) {
-      run = dmin(run, Es[min(t, tlim)]);
+      run = vmin(run, Es[min(t, tlim)]);
       sf[t] = run;
     }
-    double totS = run;
-    run = PST_INF;
+    V totS = run;
+    run = VT<V>::inf();
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      run = dmin(run, Ep[min(t, tlim)]);
+      run = vmin(run, Ep[min(t, tlim)]);
       pr[t] = run;
     }
-    double totP = run;
+    V totP = run;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       if (off < g.LPB) {
-        const double ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
-        const double dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
-        totS = dmin(totS, ds);
-        totP = dmin(totP, dp);
+        const V ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
+        const V dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
+        totS = vmin(totS, ds);
+        totP = vmin(totP, dp);
       }
     }
-    double cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
-    double cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
-    if (g.ll == g.LPB - 1) cs = PST_INF;
-    if (g.ll == 0) cp = PST_INF;
-    const double C = dmin(cs, cp);
+    V cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
+    V cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
+    if (g.ll == g.LPB - 1) cs = VT<V>::inf();
+    if (g.ll == 0) cp = VT<V>::inf();
+    const V C = vmin(cs, cp);
     if (live) {
-      double* st = srow + bb;
+      V* st = srow + bb;
 #pragma unroll
       for (int t = 0; t < CH; ++t) {
         const int u = g.u0 + t;
-        if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
+        if (u < w) st[u] = (t > 0) ? vmin(vmin(sf[t], C), pr[t - 1]) : vmin(sf[t], C);
       }
     }
   }
@@ -242,54 +289,54 @@ __device__ __forceinline__ void vh_row_reg(const double* __restrict__ E, int w, 
 
 // Two rows per barrier: 2*nblk (row, block) tasks over the lane groups, so
 // that long windows (few blocks per tile) keep more warps busy.
-template <int CH>
-__device__ __forceinline__ void vh_rows2_reg(const double* __restrict__ E0, const double* __restrict__ E1,
-                                             int ntask, int w, const VHGeom& g, int warp, int nw,
-                                             double* __restrict__ S0, double* __restrict__ S1) {
+template <int CH, class V>
+__device__ __forceinline__ void vh_rows2_reg(const V* __restrict__ E0, const V* __restrict__ E1, int ntask, int w,
+                                             const VHGeom& g, int warp, int nw, V* __restrict__ S0,
+                                             V* __restrict__ S1) {
   for (int t0 = warp * g.bpw; t0 < ntask; t0 += nw * g.bpw) {  // warp-uniform trip count
     const int tau = t0 + g.sub;
     const bool live = tau < ntask;
     const bool second = tau >= g.nblk;
-    const double* E = second ? E1 : E0;
+    const V* E = second ? E1 : E0;
     const int bb = (second ? tau - g.nblk : tau) * w, bn = bb + w;
-    const double* Es = E + (live ? bb : 0) + g.u0;  // clamped reads, as in vh_row_reg
-    const double* Ep = E + (live ? bn : w) + g.u0;
+    const V* Es = E + (live ? bb : 0) + g.u0;  // clamped reads, as in vh_row_reg
+    const V* Ep = E + (live ? bn : w) + g.u0;
     const int tlim = w - 1 - g.u0;
-    double sf[CH], pr[CH];
-    double run = PST_INF;
+    V sf[CH], pr[CH];
+    V run = VT<V>::inf();
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t) {
-      run = dmin(run, Es[min(t, tlim)]);
+      run = vmin(run, Es[min(t, tlim)]);
       sf[t] = run;
     }
-    double totS = run;
-    run = PST_INF;
+    V totS = run;
+    run = VT<V>::inf();
 #pragma unroll
     for (int t = 0; t < CH; ++t) {
-      run = dmin(run, Ep[min(t, tlim)]);
+      run = vmin(run, Ep[min(t, tlim)]);
       pr[t] = run;
     }
-    double totP = run;
+    V totP = run;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       if (off < g.LPB) {
-        const double ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
-        const double dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
-        totS = dmin(totS, ds);
-        totP = dmin(totP, dp);
+        const V ds = __shfl_down_sync(FULLMASK, totS, off, g.LPB);
+        const V dp = __shfl_up_sync(FULLMASK, totP, off, g.LPB);
+        totS = vmin(totS, ds);
+        totP = vmin(totP, dp);
       }
     }
-    double cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
-    double cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
-    if (g.ll == g.LPB - 1) cs = PST_INF;
-    if (g.ll == 0) cp = PST_INF;
-    const double C = dmin(cs, cp);
+    V cs = __shfl_down_sync(FULLMASK, totS, 1, g.LPB);
+    V cp = __shfl_up_sync(FULLMASK, totP, 1, g.LPB);
+    if (g.ll == g.LPB - 1) cs = VT<V>::inf();
+    if (g.ll == 0) cp = VT<V>::inf();
+    const V C = vmin(cs, cp);
     if (live) {
-      double* st = (second ? S1 : S0) + bb;
+      V* st = (second ? S1 : S0) + bb;
 #pragma unroll
       for (int t = 0; t < CH; ++t) {
         const int u = g.u0 + t;
-        if (u < w) st[u] = (t > 0) ? dmin(dmin(sf[t], C), pr[t - 1]) : dmin(sf[t], C);
+        if (u < w) st[u] = (t > 0) ? vmin(vmin(sf[t], C), pr[t - 1]) : vmin(sf[t], C);
       }
     }
   }
@@ -298,11 +345,11 @@ __device__ __forceinline__ void vh_rows2_reg(const double* __restrict__ E0, cons
 // One AB row from the CTA row buffer to HBM in lane-run order: window
 // j = L*R + r (L = 0..31, r = 0..R-1) is stored at r*32 + L, so that the 32
 // lanes of a selection warp, which sweep windows L*R + r for r = 0, 1, ...,
-// read one contiguous 256-byte line per row.  Thread tid always moves the
-// same positions (lane L = tid%32, r = tid/32 + c*NT/32), so the offsets are
-// set up once per tile and each element is one LDS + one STG; shared reads
-// srow[L*R + r] have odd stride R (bank-conflict free), global stores are
-// contiguous.  At most MAXC = P+1 elements per thread (T <= NT*P).
+// read one contiguous 32-value line per row and step.  Thread tid always
+// moves the same positions (lane L = tid%32, r = tid/32 + c*NT/32), so the
+// offsets are set up once per tile and each element is one LDS + one STG;
+// shared reads srow[L*R + r] have odd stride R (bank-conflict free), global
+// stores are contiguous.  At most MAXC = P+1 elements per thread (T <= NT*P).
 struct AbStore {
   int src, dst, cnt;
 };
@@ -316,11 +363,10 @@ __device__ __forceinline__ AbStore ab_store_setup(int NJ, int R, int tid) {
   s.cnt = j0 < jend ? (jend - j0 + NT / 32 - 1) / (NT / 32) : 0;
   return s;
 }
-template <int NT, int MAXC>
-__device__ __forceinline__ void store_ab_row(const AbStore& g, const double* __restrict__ srow,
-                                             double* __restrict__ dst) {
-  const double* s = srow + g.src;
-  double* d = dst + g.dst;
+template <int NT, int MAXC, class V>
+__device__ __forceinline__ void store_ab_row(const AbStore& g, const V* __restrict__ srow, V* __restrict__ dst) {
+  const V* s = srow + g.src;
+  V* d = dst + g.dst;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c)
     if (c < g.cnt) d[c * NT] = s[c * (NT / 32)];
@@ -350,9 +396,10 @@ __device__ __forceinline__ void split_task(const SplitGeom& sg, int t, int w, in
   hi = min(lo + sg.L, end);
 }
 // phase 1: part-local scans; TOT[(suf ? 0 : 1) * 32 * 16 + b * 16 + q] = part minimum
-__device__ __forceinline__ void vh_split_scan(const double* __restrict__ E, double* __restrict__ SUF,
-                                              double* __restrict__ PRE, double* __restrict__ TOT,
-                                              const SplitGeom& sg, int w, int NC, int warp, int lane, int nw) {
+template <class V>
+__device__ __forceinline__ void vh_split_scan(const V* __restrict__ E, V* __restrict__ SUF, V* __restrict__ PRE,
+                                              V* __restrict__ TOT, const SplitGeom& sg, int w, int NC, int warp,
+                                              int lane, int nw) {
   for (int t = warp; t < sg.ntask; t += nw) {
     bool suf;
     int b, q, lo, hi;
@@ -360,69 +407,85 @@ __device__ __forceinline__ void vh_split_scan(const double* __restrict__ E, doub
     const int len = hi - lo;
     const int ch = (len + 31) >> 5;
     const int u0 = lo + lane * ch, u1 = min(u0 + ch, hi);
-    double run = PST_INF;
+    V run = VT<V>::inf();
     if (suf) {
       for (int c = u1 - 1; c >= u0; --c) {
-        run = dmin(run, E[c]);
+        run = vmin(run, E[c]);
         SUF[c] = run;
       }
     } else {
       for (int c = u0; c < u1; ++c) {
-        run = dmin(run, E[c]);
+        run = vmin(run, E[c]);
         PRE[c] = run;
       }
     }
-    double tot = run;  // carry between lanes of the part
+    V tot = run;  // carry between lanes of the part
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const double o = suf ? __shfl_down_sync(FULLMASK, tot, off) : __shfl_up_sync(FULLMASK, tot, off);
-      if (suf ? lane + off < 32 : lane >= off) tot = dmin(tot, o);
+      const V o = suf ? __shfl_down_sync(FULLMASK, tot, off) : __shfl_up_sync(FULLMASK, tot, off);
+      if (suf ? lane + off < 32 : lane >= off) tot = vmin(tot, o);
     }
-    double carry = suf ? __shfl_down_sync(FULLMASK, tot, 1) : __shfl_up_sync(FULLMASK, tot, 1);
-    if (suf ? lane == 31 : lane == 0) carry = PST_INF;
+    V carry = suf ? __shfl_down_sync(FULLMASK, tot, 1) : __shfl_up_sync(FULLMASK, tot, 1);
+    if (suf ? lane == 31 : lane == 0) carry = VT<V>::inf();
     if (suf)
-      for (int c = u0; c < u1; ++c) SUF[c] = dmin(SUF[c], carry);
+      for (int c = u0; c < u1; ++c) SUF[c] = vmin(SUF[c], carry);
     else
-      for (int c = u0; c < u1; ++c) PRE[c] = dmin(PRE[c], carry);
+      for (int c = u0; c < u1; ++c) PRE[c] = vmin(PRE[c], carry);
     // part minimum: lane 0 holds the suffix over the whole part, lane 31 the prefix
-    const double pm = __shfl_sync(FULLMASK, tot, suf ? 0 : 31);
+    const V pm = __shfl_sync(FULLMASK, tot, suf ? 0 : 31);
     if (lane == 0) TOT[(suf ? 0 : 512) + b * 16 + q] = pm;
   }
 }
 // phase 2: carries from the other parts of the same block
-__device__ __forceinline__ void vh_split_carry(double* __restrict__ SUF, double* __restrict__ PRE,
-                                               const double* __restrict__ TOT, const SplitGeom& sg, int w, int NC,
-                                               int warp, int lane, int nw) {
+template <class V>
+__device__ __forceinline__ void vh_split_carry(V* __restrict__ SUF, V* __restrict__ PRE, const V* __restrict__ TOT,
+                                               const SplitGeom& sg, int w, int NC, int warp, int lane, int nw) {
   for (int t = warp; t < sg.ntask; t += nw) {
     bool suf;
     int b, q, lo, hi;
     split_task(sg, t, w, NC, suf, b, q, lo, hi);
     if (suf ? q == sg.Q - 1 : q == 0) continue;  // no parts beyond (SUF) / before (PRE)
-    double v = PST_INF;
+    V v = VT<V>::inf();
     if (lane < sg.Q && (suf ? lane > q : lane < q)) v = TOT[(suf ? 0 : 512) + b * 16 + lane];
-    const double carry = warp_min(v);
+    const V carry = warp_min(v);
     if (suf)
-      for (int c = lo + lane; c < hi; c += 32) SUF[c] = dmin(SUF[c], carry);
+      for (int c = lo + lane; c < hi; c += 32) SUF[c] = vmin(SUF[c], carry);
     else
-      for (int c = lo + lane; c < hi; c += 32) PRE[c] = dmin(PRE[c], carry);
+      for (int c = lo + lane; c < hi; c += 32) PRE[c] = vmin(PRE[c], carry);
   }
 }
 // deferred store of a long-window row: AB[j] = min(SUF[j], PRE[j + w - 1]) in lane-run order
-template <int NT, int MAXC>
-__device__ __forceinline__ void store_ab_combine(const AbStore& g, const double* __restrict__ SUF,
-                                                 const double* __restrict__ PREw, double* __restrict__ dst) {
-  const double* s = SUF + g.src;
-  const double* p = PREw + g.src;
-  double* d = dst + g.dst;
+template <int NT, int MAXC, class V>
+__device__ __forceinline__ void store_ab_combine(const AbStore& g, const V* __restrict__ SUF,
+                                                 const V* __restrict__ PREw, V* __restrict__ dst) {
+  const V* s = SUF + g.src;
+  const V* p = PREw + g.src;
+  V* d = dst + g.dst;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c)
-    if (c < g.cnt) d[c * NT] = dmin(s[c * (NT / 32)], p[c * (NT / 32)]);
+    if (c < g.cnt) d[c * NT] = vmin(s[c * (NT / 32)], p[c * (NT / 32)]);
 }
 
-template <int P, int NT, int CHM>
+__host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+// Dynamic shared memory of the one-row kernel (k_mpdist): doubles first
+// (row-0 staging xs[l], left-edge dots, per-row scalars, warp exchange), then
+// the V arrays (e rows, AB row buffers; long windows: split van Herk buffers).
+__host__ __device__ inline size_t smem_row1(bool klong, int64_t l, int64_t w, int64_t ncm, size_t sv) {
+  if (!klong) return align16((size_t)(l + 4 * w + 66) * 8) + (size_t)(4 * ncm) * sv;
+  size_t b = align16((size_t)(w + 66) * 8) + (size_t)(6 * ncm + 1024) * sv;
+  if ((size_t)l * 8 > (size_t)ncm * sv) b = align16(b) + (size_t)l * 8;  // xs does not fit E1
+  return b;
+}
+// two rows per barrier (k_mpdist2)
+__host__ __device__ inline size_t smem_row2(int64_t l, int64_t w, int64_t ncm, size_t sv) {
+  return align16((size_t)(l + 4 * w + 130) * 8) + (size_t)(8 * ncm) * sv;
+}
+
+template <int P, int NT, int CHM, class V>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <= 256 ? 2 : 1))
     k_mpdist(const MPArgs a) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   constexpr int NCmax = NT * P;
@@ -433,34 +496,41 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   const int NC = NJ + w - 1;
   // Long windows (CHM == 0, shared-memory van Herk) keep only edge[] of the
   // per-row arrays in shared memory -- their row scalars come from global
-  // memory (L1 broadcast) -- and stage xs in E1 (unused until row 1), so a
-  // tile can hold P = 7 columns per thread.
+  // memory (L1 broadcast) -- and stage xs in E1 (unused until row 1) when it
+  // fits, so a tile can hold P = 7 columns per thread.
   constexpr bool kLong = (CHM == 0);
-  double *xs, *edge, *rdf = nullptr, *rdg = nullptr, *rnq = nullptr, *E0;
-  if constexpr (!kLong) {
-    xs = sm;                   // [l]
-    edge = xs + l;             // [w]
-    rdf = edge + w;            // [w] df[q-1] per row
-    rdg = rdf + w;             // [w] dg[q-1] per row
-    rnq = rdg + w;             // [w] nrm[q] per row
-    E0 = rnq + w;              // [NCmax] row e-values (even rows), later allP_BA
-  } else {
-    edge = sm;
-    E0 = edge + w;
+  double *xs = nullptr, *edge, *rdf = nullptr, *rdg = nullptr, *rnq = nullptr, *xfer, *red;
+  {
+    double* db = (double*)smraw;
+    if constexpr (!kLong) {
+      xs = db;               // [l]
+      edge = xs + l;         // [w]
+      rdf = edge + w;        // [w] df[q-1] per row
+      rdg = rdf + w;         // [w] dg[q-1] per row
+      rnq = rdg + w;         // [w] nrm[q] per row
+      xfer = rnq + w;        // [64]
+    } else {
+      edge = db;
+      xfer = edge + w;
+    }
+    red = xfer + 64;         // [2]
   }
-  double* E1 = E0 + NCmax;     // [NCmax] row e-values (odd rows)
-  double* xfer = E1 + NCmax;   // [64]
-  double* red = xfer + 64;     // [2]
-  double* SR0 = red + 2;        // [NCmax] AB row buffer (even rows)
-  double* SR1 = SR0 + NCmax;    // [NCmax] AB row buffer (odd rows)
-  double* SUF = SR1 + NCmax;    // [NCmax] (shared-memory van Herk only)
-  double* PRE = SUF + NCmax;    // [NCmax]
-  double* TOT = PRE + NCmax;    // [1024] part minima of the split van Herk (long windows)
-  if constexpr (kLong) xs = (l <= NCmax) ? E1 : TOT + 1024;
-  double* E = E0;
+  V* E0 = (V*)(smraw + align16((size_t)((kLong ? w : l + 4 * w) + 66) * 8));  // [NCmax] e rows (even), later allP_BA
+  V* E1 = E0 + NCmax;        // [NCmax] row e-values (odd rows)
+  V* SR0 = E1 + NCmax;       // [NCmax] AB row buffer (even rows)
+  V* SR1 = SR0 + NCmax;      // [NCmax] AB row buffer (odd rows)
+  V* SUF = SR1 + NCmax;      // [NCmax] (shared-memory van Herk only)
+  V* PRE = SUF + NCmax;      // [NCmax]
+  V* TOT = PRE + NCmax;      // [1024] part minima of the split van Herk (long windows)
+  if constexpr (kLong)
+    xs = ((size_t)l * 8 <= (size_t)NCmax * sizeof(V)) ? (double*)E1
+                                                       : (double*)((unsigned char*)smraw + align16(
+                                                             align16((size_t)(w + 66) * 8) +
+                                                             (size_t)(6 * NCmax + 1024) * sizeof(V)));
+  V* E = E0;
   // AB scratch of this CTA: [w][Tp], each row in lane-run order (store_ab_row)
   const int R = (int)a.R, Tp = (int)a.Tp;
-  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
+  V* ab = (V*)a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
   const double* __restrict__ xJ = a.x + J0;
   const double* __restrict__ xQ = a.x + q0;
   const double* __restrict__ muJ = a.mu + J0;
@@ -521,7 +591,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     }
   }
   // ---- per-column constants
-  double dgc[P], dfc[P], nrmc[P], bic[P], colmin[P];
+  double dgc[P], dfc[P], nrmc[P], bic[P];
+  V colmin[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const int cl = tid * P + p;
@@ -531,7 +602,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     dfc[p] = (ok && c > 0) ? a.df[c - 1] : 0.0;
     nrmc[p] = ok ? a.nrm[c] : 0.0;
     bic[p] = ok ? a.bias[c] : PST_INF;
-    colmin[p] = PST_INF;
+    colmin[p] = VT<V>::inf();
   }
   __syncthreads();
 
@@ -571,49 +642,50 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     if (lane == 31) xfer[(i & 1) * 32 + warp] = cov[P - 1];
     const double nq = kLong ? __ldg(a.nrm + q0 + i) : rnq[i];
     E = (i & 1) ? E1 : E0;
-    double* Et = E + tid * P;
+    V* Et = E + tid * P;
     if (nq != 0.0) {
       const double mnq = -nq;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const double e = fma(cov[p] * mnq, nrmc[p], bic[p]);
-        colmin[p] = dmin(colmin[p], e);
+        const V e = VT<V>::of(fma(cov[p] * mnq, nrmc[p], bic[p]));
+        colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
       if (tail) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-          if (tid * P + p >= NC) Et[p] = PST_INF;
+          if (tid * P + p >= NC) Et[p] = VT<V>::inf();
       }
     } else {  // constant query window (row-uniform branch): zdist.py:111-112
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const int cl = tid * P + p;
-        const double e = (cl < NC) ? a.cbias[J0 + cl] : PST_INF;
-        colmin[p] = dmin(colmin[p], e);
+        const V e = (cl < NC) ? VT<V>::of(a.cbias[J0 + cl]) : VT<V>::inf();
+        colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
     }
     {  // self column (zdist.py:121-122)
       const int ql = qloc + i;
-      if (ql >= 0 && ql < P) Et[ql] = 0.0;
+      if (ql >= 0 && ql < P) Et[ql] = VT<V>::of(0.0);
     }
     __syncthreads();
     if constexpr (CHM > 0) {
       // the previous row's AB values are complete (written before this barrier)
-      if (i > 0) store_ab_row<NT, P + 1>(abst, (i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp);
-      vh_row_reg<CHM>(E, w, g, warp, NW, (i & 1) ? SR1 : SR0);
+      if (i > 0) store_ab_row<NT, P + 1, V>(abst, (i & 1) ? SR0 : SR1, ab + (int64_t)(i - 1) * Tp);
+      vh_row_reg<CHM, V>(E, w, g, warp, NW, (i & 1) ? SR1 : SR0);
     } else {
       // buffers by row parity: (SUF, PRE) = (SUF, PRE) for even rows, (SR0, SR1) for odd rows
       if (i > 0) {
         const bool po = (i - 1) & 1;
-        store_ab_combine<NT, P + 1>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1), ab + (int64_t)(i - 1) * Tp);
+        store_ab_combine<NT, P + 1, V>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1),
+                                       ab + (int64_t)(i - 1) * Tp);
       }
-      double* sufc = (i & 1) ? SR0 : SUF;
-      double* prec = (i & 1) ? SR1 : PRE;
-      vh_split_scan(E, sufc, prec, TOT, sg, w, NC, warp, lane, NW);
+      V* sufc = (i & 1) ? SR0 : SUF;
+      V* prec = (i & 1) ? SR1 : PRE;
+      vh_split_scan<V>(E, sufc, prec, TOT, sg, w, NC, warp, lane, NW);
       __syncthreads();  // part totals complete
-      vh_split_carry(sufc, prec, TOT, sg, w, NC, warp, lane, NW);
+      vh_split_carry<V>(sufc, prec, TOT, sg, w, NC, warp, lane, NW);
     }
     // no trailing barrier: the next row writes the other E / row buffers; the
     // barrier after that row's writes orders this row's reads before row i+2's writes.
@@ -621,10 +693,10 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   }
   __syncthreads();
   if constexpr (CHM > 0) {
-    store_ab_row<NT, P + 1>(abst, ((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp);
+    store_ab_row<NT, P + 1, V>(abst, ((w - 1) & 1) ? SR1 : SR0, ab + (int64_t)(w - 1) * Tp);
   } else {
     const bool po = (w - 1) & 1;
-    store_ab_combine<NT, P + 1>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1), ab + (int64_t)(w - 1) * Tp);
+    store_ab_combine<NT, P + 1, V>(abst, po ? SR0 : SUF, (po ? SR1 : PRE) + (w - 1), ab + (int64_t)(w - 1) * Tp);
   }
   E = E0;
 
@@ -633,14 +705,14 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   for (int p = 0; p < P; ++p) {
     const int cl = tid * P + p;
     const int64_t c = J0 + cl;
-    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : colmin[p];
+    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? VT<V>::of(0.0) : colmin[p];
   }
   __syncthreads();
   {
-    double* bag = a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
+    V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
     for (int c = tid; c < NC; c += NT) bag[c] = E[c];
     if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
-      for (int c = tid; c < NC; c += NT) a.dbg_ba[c] = E[c];
+      for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = E[c];
   }
 }
 
@@ -651,10 +723,10 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
 // shared memory from the previous warp), the ghost is advanced with the first
 // row, and the second row uses it.  Same arithmetic as k_mpdist (bit-identical
 // e values); half the barriers and twice the van Herk tasks per phase.
-template <int P, int NT, int CHM>
+template <int P, int NT, int CHM, class V>
 __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(const MPArgs a) {
   static_assert(CHM > 0, "two-row kernel uses the register van Herk");
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = NT / 32;
   constexpr int NCmax = NT * P;
@@ -663,17 +735,17 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
-  double* xs = sm;               // [l]
+  double* xs = (double*)smraw;   // [l]
   double* edge = xs + l;         // [w]
   double* rdf = edge + w;        // [w] df[q-1] per row
   double* rdg = rdf + w;         // [w] dg[q-1] per row
   double* rnq = rdg + w;         // [w] nrm[q] per row
-  double* EB = rnq + w;          // [4][NCmax] e rows: (pair parity, row of pair); later allP_BA
-  double* SRB = EB + 4 * NCmax;  // [4][NCmax] AB row buffers
-  double* xfer = SRB + 4 * NCmax;  // [2 parity][2][32] last two covariances of each warp
+  double* xfer = rnq + w;        // [2 parity][2][32] last two covariances of each warp
   double* red = xfer + 128;      // [2]
+  V* EB = (V*)(smraw + align16((size_t)(l + 4 * w + 130) * 8));  // [4][NCmax] e rows; later allP_BA
+  V* SRB = EB + 4 * NCmax;       // [4][NCmax] AB row buffers
   const int R = (int)a.R, Tp = (int)a.Tp;
-  double* ab = a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
+  V* ab = (V*)a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
   const double* __restrict__ xJ = a.x + J0;
   const double* __restrict__ xQ = a.x + q0;
   const double* __restrict__ muJ = a.mu + J0;
@@ -730,7 +802,8 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
     rnq[i] = a.nrm[q0 + i];
   }
-  double dgc[P], dfc[P], nrmc[P], bic[P], colmin[P];
+  double dgc[P], dfc[P], nrmc[P], bic[P];
+  V colmin[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const int cl = tid * P + p;
@@ -740,7 +813,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     dfc[p] = (ok && c > 0) ? a.df[c - 1] : 0.0;
     nrmc[p] = ok ? a.nrm[c] : 0.0;
     bic[p] = ok ? a.bias[c] : PST_INF;
-    colmin[p] = PST_INF;
+    colmin[p] = VT<V>::inf();
   }
   // ghost column c0-1 (c0 = J0 + tid*P): its recurrence constants
   double dgG = 0.0, dfG = 0.0;
@@ -774,32 +847,32 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   const AbStore abst = ab_store_setup<NT>(NJ, R, tid);
 
   // e-values of one row from its covariances -> shared row, column minima
-  auto emit_row = [&](const double* cv, int i, double* Et) {
+  auto emit_row = [&](const double* cv, int i, V* Et) {
     const double nq = rnq[i];
     if (nq != 0.0) {
       const double mnq = -nq;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const double e = fma(cv[p] * mnq, nrmc[p], bic[p]);
-        colmin[p] = dmin(colmin[p], e);
+        const V e = VT<V>::of(fma(cv[p] * mnq, nrmc[p], bic[p]));
+        colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
       if (tail) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-          if (tid * P + p >= NC) Et[p] = PST_INF;
+          if (tid * P + p >= NC) Et[p] = VT<V>::inf();
       }
     } else {  // constant query window (row-uniform branch): zdist.py:111-112
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const int cl = tid * P + p;
-        const double e = (cl < NC) ? a.cbias[J0 + cl] : PST_INF;
-        colmin[p] = dmin(colmin[p], e);
+        const V e = (cl < NC) ? VT<V>::of(a.cbias[J0 + cl]) : VT<V>::inf();
+        colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
     }
     const int ql = qloc + i;  // self column (zdist.py:121-122)
-    if (ql >= 0 && ql < P) Et[ql] = 0.0;
+    if (ql >= 0 && ql < P) Et[ql] = VT<V>::of(0.0);
   };
 
   const int npair = (w + 1) / 2;
@@ -842,102 +915,107 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     __syncthreads();
     if (it > 0) {  // AB rows of the previous pair are complete
       const int pp = par ^ 1;
-      store_ab_row<NT, P + 1>(abst, SRB + (pp * 2 + 0) * NCmax, ab + (int64_t)(i0 - 2) * Tp);
-      store_ab_row<NT, P + 1>(abst, SRB + (pp * 2 + 1) * NCmax, ab + (int64_t)(i0 - 1) * Tp);
+      store_ab_row<NT, P + 1, V>(abst, SRB + (pp * 2 + 0) * NCmax, ab + (int64_t)(i0 - 2) * Tp);
+      store_ab_row<NT, P + 1, V>(abst, SRB + (pp * 2 + 1) * NCmax, ab + (int64_t)(i0 - 1) * Tp);
     }
-    vh_rows2_reg<CHM>(EB + (par * 2 + 0) * NCmax, EB + (par * 2 + 1) * NCmax, g.nblk * (has1 ? 2 : 1), w, g,
-                      warp, NW, SRB + (par * 2 + 0) * NCmax, SRB + (par * 2 + 1) * NCmax);
+    vh_rows2_reg<CHM, V>(EB + (par * 2 + 0) * NCmax, EB + (par * 2 + 1) * NCmax, g.nblk * (has1 ? 2 : 1), w, g,
+                         warp, NW, SRB + (par * 2 + 0) * NCmax, SRB + (par * 2 + 1) * NCmax);
   }
   __syncthreads();
   {
     const int it = npair - 1, par = it & 1, i0 = 2 * it;
-    store_ab_row<NT, P + 1>(abst, SRB + (par * 2 + 0) * NCmax, ab + (int64_t)i0 * Tp);
-    if (i0 + 1 < w) store_ab_row<NT, P + 1>(abst, SRB + (par * 2 + 1) * NCmax, ab + (int64_t)(i0 + 1) * Tp);
+    store_ab_row<NT, P + 1, V>(abst, SRB + (par * 2 + 0) * NCmax, ab + (int64_t)i0 * Tp);
+    if (i0 + 1 < w) store_ab_row<NT, P + 1, V>(abst, SRB + (par * 2 + 1) * NCmax, ab + (int64_t)(i0 + 1) * Tp);
   }
-  double* E = EB;  // allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
+  V* E = EB;  // allP_BA (column minima), clamped; self columns [q0, q0+w) are exactly 0
 #pragma unroll
   for (int p = 0; p < P; ++p) {
     const int cl = tid * P + p;
     const int64_t c = J0 + cl;
-    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? 0.0 : colmin[p];
+    if (cl < NC) E[cl] = (c >= q0 && c < q0 + w) ? VT<V>::of(0.0) : colmin[p];
   }
   __syncthreads();
   {
-    double* bag = a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
+    V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
     for (int c = tid; c < NC; c += NT) bag[c] = E[c];
     if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
-      for (int c = tid; c < NC; c += NT) a.dbg_ba[c] = E[c];
+      for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = E[c];
   }
 }
 
 // Generic (memory-resident) variant of the warp selection for 2w > 32*2*16.
+template <class V>
 struct MemWin {
-  const double* A;  // row minima, stride sa
-  const double* B;  // column minima, contiguous
+  const V* A;  // row minima, stride sa
+  const V* B;  // column minima, contiguous
   int w;
   int64_t sa;
 };
-__device__ __forceinline__ void count2m(const MemWin& v, int lane, double p, int& lt, int& le) {
+template <class V>
+__device__ __forceinline__ void count2m(const MemWin<V>& v, int lane, V p, int& lt, int& le) {
   int l1 = 0, l2 = 0;
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i * v.sa], y = v.B[i];
+    const V x = v.A[i * v.sa], y = v.B[i];
     l1 += (x < p) + (y < p);
     l2 += (x <= p) + (y <= p);
   }
   lt = __reduce_add_sync(FULLMASK, l1);
   le = __reduce_add_sync(FULLMASK, l2);
 }
-__device__ __forceinline__ double below_maxm(const MemWin& v, int lane, double p) {
-  double m = -PST_INF;
+template <class V>
+__device__ __forceinline__ V below_maxm(const MemWin<V>& v, int lane, V p) {
+  V m = VT<V>::ninf();
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i * v.sa], y = v.B[i];
-    m = dmax(m, x < p ? x : -PST_INF);
-    m = dmax(m, y < p ? y : -PST_INF);
+    const V x = v.A[i * v.sa], y = v.B[i];
+    m = vmax(m, x < p ? x : VT<V>::ninf());
+    m = vmax(m, y < p ? y : VT<V>::ninf());
   }
   return warp_max(m);
 }
-__device__ __forceinline__ double above_minm(const MemWin& v, int lane, double p) {
-  double m = PST_INF;
+template <class V>
+__device__ __forceinline__ V above_minm(const MemWin<V>& v, int lane, V p) {
+  V m = VT<V>::inf();
   for (int i = lane; i < v.w; i += 32) {
-    const double x = v.A[i * v.sa], y = v.B[i];
-    m = dmin(m, x > p ? x : PST_INF);
-    m = dmin(m, y > p ? y : PST_INF);
+    const V x = v.A[i * v.sa], y = v.B[i];
+    m = vmin(m, x > p ? x : VT<V>::inf());
+    m = vmin(m, y > p ? y : VT<V>::inf());
   }
   return warp_min(m);
 }
-__device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, int lt0 = -1, int le0 = -1) {
+template <class V>
+__device__ V warp_select_mem(const MemWin<V>& v, int lane, int k, V p, int lt0 = -1, int le0 = -1) {
   const int w = v.w;
-  double lov = -PST_INF, hi = PST_INF;
+  V lov = VT<V>::ninf(), hi = VT<V>::inf();
   int clo = 0, chi = 2 * w, grow = 0;
   bool haveLo = false, haveHi = false;
-  for (int it = 0; it < 256; ++it) {
+  for (int it = 0; it < 2 * w + 2; ++it) {  // >= 1 element leaves the bracket per iteration
     int lt, le;
     if (it == 0 && lt0 >= 0) {
       lt = lt0;
       le = le0;
     } else {
-      count2m(v, lane, p, lt, le);
+      count2m<V>(v, lane, p, lt, le);
     }
     if (lt < k && k <= le) return p;
     const bool down = k <= lt;
-    double nv;
+    V nv;
     int dist;
     if (down) {
-      nv = below_maxm(v, lane, p);
+      nv = below_maxm<V>(v, lane, p);
       if (k == lt) return nv;
       hi = nv;
       chi = lt;
       haveHi = true;
       dist = lt - k;
     } else {
-      nv = above_minm(v, lane, p);
+      nv = above_minm<V>(v, lane, p);
       if (k == le + 1) return nv;
       lov = nv;
       clo = le;
       haveLo = true;
       dist = k - le - 1;
     }
-    p = next_pivot(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
+    p = next_pivot<V>(it, down, dist, p, nv, lov, hi, clo, chi, k, haveLo, haveHi, grow);
   }
   return p;
 }
@@ -946,7 +1024,7 @@ __device__ double warp_select_mem(const MemWin& v, int lane, int k, double p, in
 // NWS warps.  Lane L of a warp owns the run of consecutive windows
 // j = L*R + r, r in [r0, r1) (the warp's share of the run length R); the AB
 // scratch is stored in lane-run order, so at step r the warp's 32 lanes read
-// one contiguous 256-byte line per row, and lane L's column-minima window
+// one contiguous line per row, and lane L's column-minima window
 // BA[j .. j+w) in shared memory has lane stride R (odd: conflict free).
 //
 // Step r: every lane counts #(< p) and #(<= p) of its own 2w values with the
@@ -962,30 +1040,42 @@ __device__ __forceinline__ double e_to_dist(double ev, double twol) {
   if (ev > 2.0) ev = 2.0;    // rho clipped at -1 (zdist.py:117)
   return sqrt(twol * ev);
 }
+// profile output: exact path d = f(e) (double rows), key path: the key itself (int rows)
+__device__ __forceinline__ void put_out(double* row, int64_t j, double v, double twol) { row[j] = e_to_dist(v, twol); }
+__device__ __forceinline__ void put_out(int* row, int64_t j, int v, double) { row[j] = v; }
+template <class V>
+struct OutT {
+  using type = double;
+};
+template <>
+struct OutT<int> {
+  using type = int;
+};
 
 // exact k-th smallest of window (lane L, step r), whole warp; TM = 0: long
 // windows, values re-read from memory on every pass.  fresh: no pivot yet
 // (answers may be tiny negative residues, so no sentinel value is used).
 // Also returns #(B < ans) and #(B <= ans) for the lane's incremental B counts.
-template <int TM>
-__device__ __forceinline__ double solve_window(const double* __restrict__ ab, const double* BA, int w, int k,
-                                               int R, int Tp, int L, int r, int lane, bool fresh, double piv,
-                                               int lt0, int le0, int& ltB, int& leB, double* colbuf) {
-  const double* Ac = ab + r * 32 + L;
-  const double* Bc = BA + L * R + r;
-  double x;
+template <int TM, class V>
+__device__ __forceinline__ V solve_window(const V* __restrict__ ab, const V* BA, int w, int k, int R, int Tp, int L,
+                                          int r, int lane, bool fresh, V piv, int lt0, int le0, int& ltB, int& leB,
+                                          V* colbuf) {
+  const V* Ac = ab + r * 32 + L;
+  const V* Bc = BA + L * R + r;
+  V x;
   int b1 = 0, b2 = 0;
   if constexpr (TM > 0) {
-    WinVals<TM> v;
+    WinVals<TM, V> v;
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
       const int i = lane + 32 * t;
       const bool ok = i < w;
-      v.a[t] = ok ? __ldg(Ac + (int64_t)i * Tp) : PST_INF;
-      v.b[t] = ok ? Bc[i] : PST_INF;
+      v.a[t] = ok ? __ldg(Ac + (int64_t)i * Tp) : VT<V>::inf();
+      v.b[t] = ok ? Bc[i] : VT<V>::inf();
     }
-    if (fresh) piv = dmax(warp_max(v.a[0] < PST_INF ? v.a[0] : -PST_INF) * 0.25, 0.0);
-    x = warp_select<TM>(v, w, k, piv, lt0, le0);
+    if (fresh)
+      piv = vmax(VT<V>::quarter(warp_max(v.a[0] < VT<V>::inf() ? v.a[0] : VT<V>::ninf())), VT<V>::of(0.0));
+    x = warp_select<TM, V>(v, w, k, piv, lt0, le0);
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
       b1 += v.b[t] < x;
@@ -995,9 +1085,9 @@ __device__ __forceinline__ double solve_window(const double* __restrict__ ab, co
 #pragma unroll 8
     for (int i = lane; i < w; i += 32) colbuf[i] = __ldg(Ac + (int64_t)i * Tp);
     __syncwarp();
-    MemWin v{colbuf, Bc, w, 1};
-    if (fresh) piv = dmax(warp_max(lane < w ? colbuf[lane] : -PST_INF) * 0.25, 0.0);
-    x = warp_select_mem(v, lane, k, piv, lt0, le0);
+    MemWin<V> v{colbuf, Bc, w, 1};
+    if (fresh) piv = vmax(VT<V>::quarter(warp_max(lane < w ? colbuf[lane] : VT<V>::ninf())), VT<V>::of(0.0));
+    x = warp_select_mem<V>(v, lane, k, piv, lt0, le0);
     for (int i = lane; i < w; i += 32) {
       b1 += Bc[i] < x;
       b2 += Bc[i] <= x;
@@ -1009,23 +1099,24 @@ __device__ __forceinline__ double solve_window(const double* __restrict__ ab, co
   return x;
 }
 
-template <int NWS, int TM>
+template <int NWS, int TM, class V>
 __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int NCmax) {
-  extern __shared__ double smb[];
+  using O = typename OutT<V>::type;
+  extern __shared__ __align__(16) unsigned char smsel[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int w = (int)a.w, R = (int)a.R, Tp = (int)a.Tp, k = (int)a.k;
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  const double* __restrict__ ab = a.ab + cta * ((int64_t)w * Tp);
-  const double* __restrict__ bag = a.ba + cta * NCmax;
-  double* BA = smb;
-  double* colbuf = smb + NCmax + warp * w;  // [w] per warp, long windows (TM == 0) only
+  const V* __restrict__ ab = (const V*)a.ab + cta * ((int64_t)w * Tp);
+  const V* __restrict__ bag = (const V*)a.ba + cta * NCmax;
+  V* BA = (V*)smsel;
+  V* colbuf = BA + NCmax + warp * w;  // [w] per warp, long windows (TM == 0) only
   for (int c = tid; c < NC; c += NWS * 32) BA[c] = bag[c];
   __syncthreads();
   const double twol = 2.0 * (double)a.l;
-  double* Drow = a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
+  O* Drow = (O*)a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0;
   const int rper = (R + NWS - 1) / NWS;
   const int r0 = warp * rper, r1 = min(R, r0 + rper);
   if (r0 >= r1) return;
@@ -1035,12 +1126,12 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
     for (int r = r0; r < r1; ++r) {
       const int j = jl + r;
       const bool ok = j < NJ;
-      const double* Ap = ab + r * 32 + lane;
-      const double* Bp = BA + (ok ? j : 0);
-      double mx = -PST_INF;
+      const V* Ap = ab + r * 32 + lane;
+      const V* Bp = BA + (ok ? j : 0);
+      V mx = VT<V>::ninf();
 #pragma unroll 8
-      for (int i = 0; i < w; ++i) mx = dmax(mx, dmax(__ldg(Ap + (int64_t)i * Tp), Bp[i]));
-      if (ok) Drow[j] = e_to_dist(mx, twol);
+      for (int i = 0; i < w; ++i) mx = vmax(mx, vmax(__ldg(Ap + (int64_t)i * Tp), Bp[i]));
+      if (ok) put_out(Drow, j, mx, twol);
     }
     return;
   }
@@ -1048,28 +1139,28 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
   // first window of every lane's run, lanes in turn; lane L starts from lane
   // L-1's answer (its window lies R to the left).  ltB/leB: this lane's counts
   // of its B window (BA[j .. j+w)) below / at-or-below p, kept incrementally.
-  double p = 0.0;
+  V p = VT<V>::of(0.0);
   int ltB = 0, leB = 0;
   {
-    double prev = 0.0;
+    V prev = VT<V>::of(0.0);
     for (int L = 0; L < 32; ++L) {
       if (L * R + r0 >= NJ || (a.dbg_flags & 4)) break;  // warp-uniform
       int b1, b2;
-      prev = solve_window<TM>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2, colbuf);
+      prev = solve_window<TM, V>(ab, BA, w, k, R, Tp, L, r0, lane, L == 0, prev, -1, -1, b1, b2, colbuf);
       if (lane == L) {
         p = prev;
         ltB = b1;
         leB = b2;
       }
     }
-    if (jl + r0 < NJ) Drow[jl + r0] = e_to_dist(p, twol);
+    if (jl + r0 < NJ) put_out(Drow, jl + r0, p, twol);
   }
   for (int r = r0 + 1; r < r1; ++r) {
     const int j = jl + r;
     const bool ok = j < NJ;
-    const double* Ap = ab + r * 32 + lane;
+    const V* Ap = ab + r * 32 + lane;
     if (ok) {  // slide the B window: BA[j-1] leaves, BA[j+w-1] enters
-      const double out = BA[j - 1], in = BA[j + w - 1];
+      const V out = BA[j - 1], in = BA[j + w - 1];
       ltB += (in < p) - (out < p);
       leB += (in <= p) - (out <= p);
     }
@@ -1079,7 +1170,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
       constexpr int kSelUnroll = TM >= 7 || TM == 0 ? 32 : TM >= 4 ? 16 : 8;
 #pragma unroll kSelUnroll
       for (int i = 0; i < w; ++i) {
-        const double va = __ldg(Ap + (int64_t)i * Tp);
+        const V va = __ldg(Ap + (int64_t)i * Tp);
         lt += va < p;
         le += va <= p;
       }
@@ -1089,23 +1180,155 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
     while (pend) {
       const int L = __ffs(pend) - 1;
       pend &= pend - 1;
-      const double pl = __shfl_sync(FULLMASK, p, L);
+      const V pl = __shfl_sync(FULLMASK, p, L);
       const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
       int b1, b2;
-      const double x = solve_window<TM>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1, b2, colbuf);
+      const V x = solve_window<TM, V>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1, b2, colbuf);
       if (lane == L) {
         p = x;
         ltB = b1;
         leB = b2;
       }
     }
-    if (ok) Drow[j] = e_to_dist(p, twol);
+    if (ok) put_out(Drow, j, p, twol);
   }
 }
 
-template <int P, int NT, int CHM>
+// ---- exact profile values at single (segment, window) pairs ----------------
+// D[s][j] of the exact path, bit-identical: the window's tile (J0 = floor(j/T)*T
+// of the same TileGeom) is replayed over the diagonals that reach the w x w
+// square rows [0, w) x columns [j, j+w): row-0 fresh dots and left-edge fresh
+// dots exactly as k_mpdist computes them (same sequential sums, same fma
+// order), then the same recurrence and e formula.  One CTA per pair; the
+// diagonal state lives in a double-buffered shared row (a barrier per row).
+// Used to resolve the decisions the key path cannot certify (pastila.cu).
+struct WinArgs {
+  const double *x, *mu, *nrm, *bias, *cbias, *df, *dg;
+  int64_t l, m, w, k, N, T;
+  const int64_t *seg, *win;
+  double* out;
+};
+constexpr int WX_NT = 256;
+__global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
+  extern __shared__ __align__(16) unsigned char smw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int l = (int)a.l, w = (int)a.w, k = (int)a.k;
+  const int64_t s = a.seg[blockIdx.x], j = a.win[blockIdx.x];
+  const int64_t q0 = s * a.m;
+  const int64_t J0 = (j / a.T) * a.T;
+  const int jl = (int)(j - J0);
+  const int C0 = max(0, jl - w + 1);  // region columns [C0, jl + w) (tile-local)
+  const int NCW = jl + w - C0;
+  double* xs = (double*)smw;              // [l]
+  double* cv = xs + l;                    // [2][NCW] covariances by row parity
+  double* edge = cv + 2 * NCW;            // [w]
+  double* ABr = edge + w;                 // [w] row minima over the window
+  double* BAc = ABr + w;                  // [w] column minima of the window's columns
+  double* wmin = BAc + w;                 // [2][WX_NT/32] per-warp row minima
+  double* red = wmin + 2 * (WX_NT / 32);  // [2]
+  const double* __restrict__ xJ = a.x + J0;
+  const double* __restrict__ xQ = a.x + q0;
+  // row-0 dots (k_mpdist: acc = sum_t fma(xs[t], x[c+t]); cov = fma(-mu[c], sum xs, acc))
+  {
+    const double mq = a.mu[q0];
+    for (int t = tid; t < l; t += WX_NT) xs[t] = xQ[t] - mq;
+    __syncthreads();
+    if (tid == 0) {
+      double s1 = 0.0;
+      for (int t = 0; t < l; ++t) s1 += xs[t];
+      red[0] = s1;
+    }
+    __syncthreads();
+    const double sx = red[0];
+    for (int u = tid; u < NCW; u += WX_NT) {
+      const int cl = C0 + u;
+      const double* xc = xJ + cl;
+      double acc = 0.0;
+      for (int t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
+      cv[u] = fma(-a.mu[J0 + cl], sx, acc);
+    }
+    __syncthreads();
+  }
+  if (C0 == 0) {  // left edge column J0, rows 1..w-1
+    const double mc = a.mu[J0];
+    for (int t = tid; t < l; t += WX_NT) xs[t] = xJ[t] - mc;
+    __syncthreads();
+    if (tid == 0) {
+      double s1 = 0.0;
+      for (int t = 0; t < l; ++t) s1 += xs[t];
+      red[1] = s1;
+    }
+    __syncthreads();
+    const double sx = red[1];
+    for (int i = 1 + tid; i < w; i += WX_NT) {
+      const double* xq = xQ + i;
+      double acc = 0.0;
+      for (int t = 0; t < l; ++t) acc = fma(xq[t], xs[t], acc);
+      edge[i] = fma(-a.mu[q0 + i], sx, acc);
+    }
+  }
+  for (int u = tid; u < w; u += WX_NT) BAc[u] = PST_INF;
+  __syncthreads();
+  for (int i = 0; i < w; ++i) {
+    const double* prv = cv + ((i - 1) & 1) * NCW;
+    double* cur = cv + (i & 1) * NCW;
+    const int64_t q = q0 + i;
+    const double nq = a.nrm[q];
+    const double dfq = i > 0 ? a.df[q - 1] : 0.0, dgq = i > 0 ? a.dg[q - 1] : 0.0;
+    double rm = PST_INF;
+    for (int u = tid; u < NCW; u += WX_NT) {
+      const int cl = C0 + u;
+      const int64_t c = J0 + cl;
+      double cvv;
+      if (i == 0) {
+        cvv = cv[u];
+      } else if (cl == 0) {
+        cvv = edge[i];
+      } else {
+        const double left = u > 0 ? prv[u - 1] : 0.0;  // u == 0 (cl > 0): off the needed diagonals
+        const double dgc = c > 0 ? a.dg[c - 1] : 0.0, dfc = c > 0 ? a.df[c - 1] : 0.0;
+        cvv = fma(dfq, dgc, fma(dgq, dfc, left));
+      }
+      if (i > 0) cur[u] = cvv;
+      if (cl >= jl) {
+        double e = (nq != 0.0) ? fma(cvv * (-nq), a.nrm[c], a.bias[c]) : a.cbias[c];
+        if (c == q) e = 0.0;
+        rm = vmin(rm, e);
+        BAc[cl - jl] = vmin(BAc[cl - jl], e);  // column owned by this thread
+      }
+    }
+    rm = warp_min(rm);
+    if (lane == 0) wmin[(i & 1) * (WX_NT / 32) + warp] = rm;
+    __syncthreads();
+    if (tid == 0) {
+      double m = PST_INF;
+      for (int v = 0; v < WX_NT / 32; ++v) m = vmin(m, wmin[(i & 1) * (WX_NT / 32) + v]);
+      ABr[i] = m;
+    }
+  }
+  __syncthreads();
+  for (int u = tid; u < w; u += WX_NT) {
+    const int64_t c = j + u;
+    if (c >= q0 && c < q0 + w) BAc[u] = 0.0;  // self columns (k_mpdist allP_BA clamp)
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double ans;
+    if (2 * w <= k) {
+      double mx = -PST_INF;
+      for (int u = lane; u < w; u += 32) mx = vmax(mx, vmax(ABr[u], BAc[u]));
+      ans = warp_max(mx);
+    } else {
+      MemWin<double> v{ABr, BAc, w, 1};
+      ans = warp_select_mem<double>(v, lane, k, ABr[0], -1, -1);
+    }
+    if (lane == 0) a.out[blockIdx.x] = e_to_dist(ans, 2.0 * (double)a.l);
+  }
+}
+
+template <int P, int NT, int CHM, class V>
 int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_mpdist<P, NT, CHM>;
+  auto kern = k_mpdist<P, NT, CHM, V>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
     pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1117,10 +1340,10 @@ int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
   return PST_OK;
 }
 
-template <int NWS, int TM>
+template <int NWS, int TM, class V>
 int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
-  const size_t smem = (size_t)(NCmax + (TM == 0 ? NWS * a.w : 0)) * sizeof(double);
-  auto kern = k_select_run<NWS, TM>;
+  const size_t smem = (size_t)(NCmax + (TM == 0 ? NWS * a.w : 0)) * sizeof(V);
+  auto kern = k_select_run<NWS, TM, V>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -1136,38 +1359,39 @@ int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
 
 // warps per selection CTA: each warp's share of the run stays >= ~12 windows
 // so the warp-cooperative run starts are amortized.
-template <int TM>
+template <int TM, class V>
 int launch_sel_tm(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
   if (const char* e = getenv("PASTILA_NWS")) {  // tuning experiments
     const int v = atoi(e);
-    if (v == 1) return launch_sel_w<1, TM>(c, a, grid, NCmax);
-    if (v == 2) return launch_sel_w<2, TM>(c, a, grid, NCmax);
-    if (v == 4) return launch_sel_w<4, TM>(c, a, grid, NCmax);
+    if (v == 1) return launch_sel_w<1, TM, V>(c, a, grid, NCmax);
+    if (v == 2) return launch_sel_w<2, TM, V>(c, a, grid, NCmax);
+    if (v == 4) return launch_sel_w<4, TM, V>(c, a, grid, NCmax);
   }
-  if (a.R >= 48) return launch_sel_w<4, TM>(c, a, grid, NCmax);
-  if (a.R >= 24) return launch_sel_w<2, TM>(c, a, grid, NCmax);
-  return launch_sel_w<1, TM>(c, a, grid, NCmax);
+  if (a.R >= 48) return launch_sel_w<4, TM, V>(c, a, grid, NCmax);
+  if (a.R >= 24) return launch_sel_w<2, TM, V>(c, a, grid, NCmax);
+  return launch_sel_w<1, TM, V>(c, a, grid, NCmax);
 }
 
 // TM = ceil(w / 32) values of each half per lane in the warp-cooperative path
+template <class V>
 int launch_sel(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
   switch ((int)((a.w + 31) >> 5)) {
-    case 1: return launch_sel_tm<1>(c, a, grid, NCmax);
-    case 2: return launch_sel_tm<2>(c, a, grid, NCmax);
-    case 3: return launch_sel_tm<3>(c, a, grid, NCmax);
-    case 4: return launch_sel_tm<4>(c, a, grid, NCmax);
-    case 5: return launch_sel_tm<5>(c, a, grid, NCmax);
-    case 6: return launch_sel_tm<6>(c, a, grid, NCmax);
-    case 7: return launch_sel_tm<7>(c, a, grid, NCmax);
-    case 8: return launch_sel_tm<8>(c, a, grid, NCmax);
-    case 9: return launch_sel_tm<9>(c, a, grid, NCmax);
-    default: return launch_sel_tm<0>(c, a, grid, NCmax);
+    case 1: return launch_sel_tm<1, V>(c, a, grid, NCmax);
+    case 2: return launch_sel_tm<2, V>(c, a, grid, NCmax);
+    case 3: return launch_sel_tm<3, V>(c, a, grid, NCmax);
+    case 4: return launch_sel_tm<4, V>(c, a, grid, NCmax);
+    case 5: return launch_sel_tm<5, V>(c, a, grid, NCmax);
+    case 6: return launch_sel_tm<6, V>(c, a, grid, NCmax);
+    case 7: return launch_sel_tm<7, V>(c, a, grid, NCmax);
+    case 8: return launch_sel_tm<8, V>(c, a, grid, NCmax);
+    case 9: return launch_sel_tm<9, V>(c, a, grid, NCmax);
+    default: return launch_sel_tm<0, V>(c, a, grid, NCmax);
   }
 }
 
-template <int P, int NT, int CHM>
+template <int P, int NT, int CHM, class V>
 int launch_p2(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
-  auto kern = k_mpdist2<P, NT, CHM>;
+  auto kern = k_mpdist2<P, NT, CHM, V>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) {
     pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -1179,55 +1403,38 @@ int launch_p2(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
   return PST_OK;
 }
 
-template <int NT>
+template <int NT, class V>
 int launch_nt2(pst_ctx* c, const MPArgs& a, dim3 grid, int chm, size_t smem) {
-  if (chm == 3) return launch_p2<5, NT, 3>(c, a, grid, smem);
-  if (chm == 5) return launch_p2<5, NT, 5>(c, a, grid, smem);
-  if (chm == 7) return launch_p2<5, NT, 7>(c, a, grid, smem);
-  return launch_p2<5, NT, 9>(c, a, grid, smem);
+  if (chm == 3) return launch_p2<5, NT, 3, V>(c, a, grid, smem);
+  if (chm == 5) return launch_p2<5, NT, 5, V>(c, a, grid, smem);
+  if (chm == 7) return launch_p2<5, NT, 7, V>(c, a, grid, smem);
+  return launch_p2<5, NT, 9, V>(c, a, grid, smem);
 }
 
-template <int NT>
+template <int NT, class V>
 int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, int chm, size_t smem) {
-  if (chm == 3) return P == 5 ? launch_p<5, NT, 3>(c, a, grid, smem) : launch_p<3, NT, 3>(c, a, grid, smem);
-  if (chm == 5) return P == 5 ? launch_p<5, NT, 5>(c, a, grid, smem) : launch_p<3, NT, 5>(c, a, grid, smem);
-  if (chm == 7) return P == 5 ? launch_p<5, NT, 7>(c, a, grid, smem) : launch_p<3, NT, 7>(c, a, grid, smem);
-  if (chm == 9) return P == 5 ? launch_p<5, NT, 9>(c, a, grid, smem) : launch_p<3, NT, 9>(c, a, grid, smem);
+  if (chm == 3) return P == 5 ? launch_p<5, NT, 3, V>(c, a, grid, smem) : launch_p<3, NT, 3, V>(c, a, grid, smem);
+  if (chm == 5) return P == 5 ? launch_p<5, NT, 5, V>(c, a, grid, smem) : launch_p<3, NT, 5, V>(c, a, grid, smem);
+  if (chm == 7) return P == 5 ? launch_p<5, NT, 7, V>(c, a, grid, smem) : launch_p<3, NT, 7, V>(c, a, grid, smem);
+  if (chm == 9) return P == 5 ? launch_p<5, NT, 9, V>(c, a, grid, smem) : launch_p<3, NT, 9, V>(c, a, grid, smem);
   switch (P) {
-    case 9: return launch_p<9, NT, 0>(c, a, grid, smem);
-    case 7: return launch_p<7, NT, 0>(c, a, grid, smem);
-    case 5: return launch_p<5, NT, 0>(c, a, grid, smem);
-    case 3: return launch_p<3, NT, 0>(c, a, grid, smem);
-    default: return launch_p<1, NT, 0>(c, a, grid, smem);
+    case 9: return launch_p<9, NT, 0, V>(c, a, grid, smem);
+    case 7: return launch_p<7, NT, 0, V>(c, a, grid, smem);
+    case 5: return launch_p<5, NT, 0, V>(c, a, grid, smem);
+    case 3: return launch_p<3, NT, 0, V>(c, a, grid, smem);
+    default: return launch_p<1, NT, 0, V>(c, a, grid, smem);
   }
 }
 
 }  // namespace
 
-// Profiles of segments [seg_lo, seg_hi) into D_dev rows 0.. (row stride ld).
-static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
-                              double* D_dev, int64_t ld);
-
-int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
-                  double* D_dev, int64_t ld) {
-  PST_TRY(pst_ensure_len(c, l));
-  if (!c->timing) return launch_mpdist_impl(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
-  cudaEvent_t e0, e1;
-  PST_CUDA(cudaEventCreate(&e0));
-  PST_CUDA(cudaEventCreate(&e1));
-  PST_CUDA(cudaEventRecord(e0, c->st));
-  const int64_t before = c->launches;
-  int r = launch_mpdist_impl(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
-  PST_CUDA(cudaEventRecord(e1, c->st));
-  if (!c->tev) c->tev = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
-  ((std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev)->push_back({e0, e1});
-  c->t_launch += c->launches - before;
-  return r;
-}
-
-static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
-                              double* D_dev, int64_t ld) {
-  const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
+// Tile geometry (measured rules).  Decisions use the
+// double-valued shared-memory footprint so that both value types get the same
+// tiles, hence bit-identical e values.
+int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& G) {
+  const int64_t n = c->n, w = m - l + 1, N = n - m + 1;
+  G.w = w;
+  G.N = N;
   // tile geometry: NC = NT*P columns, T = NC - w + 1 windows; aim for T >= 4w
   int nt = (4 * w > 256 * 5) ? 512 : 256;
   if (w > 160 && w <= 288) {
@@ -1267,16 +1474,11 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     if (v == 0) chm = 0;  // split shared-memory van Herk
   }
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
-  auto smem_for = [&](int pp, int tt) {
-    const int64_t ncm = (int64_t)tt * pp;
-    if (chm == 0)  // long-window layout (k_mpdist kLong): edge + 6 rows + part minima (+ xs if not in E1)
-      return (size_t)(w + ncm * 6 + 64 + 2 + 1024 + (l > ncm ? l : 0)) * sizeof(double);
-    return (size_t)(l + 4 * w + ncm * 4 + 64 + 2) * sizeof(double);
-  };
-  if (chm == 0 && smem_for(7, nt) <= smax) P = 7;  // long windows: wider tiles (less halo)
+  auto smem_for = [&](int pp) { return smem_row1(chm == 0, l, w, (int64_t)nt * pp, 8); };
+  if (chm == 0 && smem_for(7) <= smax) P = 7;  // long windows: wider tiles (less halo)
   if (const char* e = getenv("PASTILA_P")) { const int v = atoi(e); if (v == 3 || v == 5) P = v; }  // tuning
-  while (P > 1 && smem_for(P, nt) > smax) P -= 2;
-  if (smem_for(P, nt) > smax || (int64_t)nt * P < w) {
+  while (P > 1 && smem_for(P) > smax) P -= 2;
+  if (smem_for(P) > smax || (int64_t)nt * P < w) {
     pst_set_error("snippet size %lld too large for shared-memory tiles", (long long)m);
     return PST_EINVAL;
   }
@@ -1295,13 +1497,76 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   }
   if (T > N) T = N;
   if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < T) T = v; }
-  const int64_t ntile = (N + T - 1) / T;
-  const int64_t R = ((T + 31) / 32) | 1;  // lane-run length (odd), AB row stride 32*R
-  const int64_t Tp = 32 * R;
-  // scratch: AB (S*T doubles) + allP_BA (NCmax doubles) per CTA, two buffers so the
+  G.NCmax = NCmax;
+  G.T = T;
+  G.ntile = (N + T - 1) / T;
+  G.R = ((T + 31) / 32) | 1;  // lane-run length (odd), AB row stride 32*R
+  G.Tp = 32 * G.R;
+  G.nt = nt;
+  G.P = P;
+  G.chm = chm;
+  G.smem_d = smem_for(P);
+  // two rows per barrier (k_mpdist2): register van Herk, P = 5; used when one row
+  // leaves lane-group slots idle and two rows fit one round
+  G.rows2 = false;
+  if (chm > 0 && P == 5 && smem_row2(l, w, NCmax, 8) <= smax && nt != 128) {
+    int lpb = 1;
+    while (lpb < 32 && lpb * chm < w) lpb *= 2;
+    if (lpb < 8) lpb = 8;
+    const int64_t slots = (int64_t)(nt / 32) * (32 / lpb);
+    const int64_t nblk = (std::min(T, N) + w - 1) / w;
+    G.rows2 = 2 * nblk <= slots;
+    if (const char* e = getenv("PASTILA_ROWS2")) G.rows2 = atoi(e) > 0;  // tuning experiments
+  }
+  return PST_OK;
+}
+
+// Profiles of segments [seg_lo, seg_hi) into D_dev rows 0.. (row stride ld).
+template <class V>
+static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                              void* D_dev, int64_t ld);
+
+template <class V>
+static int launch_timed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, void* D_dev,
+                        int64_t ld) {
+  PST_TRY(pst_ensure_len(c, l));
+  if (!c->timing) return launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  cudaEvent_t e0, e1;
+  PST_CUDA(cudaEventCreate(&e0));
+  PST_CUDA(cudaEventCreate(&e1));
+  PST_CUDA(cudaEventRecord(e0, c->st));
+  const int64_t before = c->launches;
+  int r = launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  PST_CUDA(cudaEventRecord(e1, c->st));
+  if (!c->tev) c->tev = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
+  ((std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev)->push_back({e0, e1});
+  c->t_launch += c->launches - before;
+  return r;
+}
+
+int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, double* D_dev,
+                  int64_t ld) {
+  return launch_timed<double>(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+}
+
+int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, int* Dk_dev,
+                       int64_t ld) {
+  return launch_timed<int>(c, m, l, k, seg_lo, seg_hi, Dk_dev, ld);
+}
+
+template <class V>
+static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
+                              void* D_dev, int64_t ld) {
+  const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
+  TileGeom G;
+  PST_TRY(tile_geom(c, m, l, G));
+  const int nt = G.nt, P = G.P, chm = G.chm;
+  const int64_t NCmax = G.NCmax, T = G.T, ntile = G.ntile, R = G.R, Tp = G.Tp;
+  constexpr size_t SV = sizeof(V);
+  // scratch: AB (w*Tp values) + allP_BA (NCmax values) per CTA, two buffers so the
   // selection of batch b (stream st2) overlaps the row loop of batch b+1 (stream st).
-  const size_t ab_cta = (size_t)w * (size_t)Tp * sizeof(double);
-  const size_t per_cta = ab_cta + (size_t)NCmax * sizeof(double);
+  const size_t ab_cta = (size_t)w * (size_t)Tp * SV;
+  const size_t per_cta = ab_cta + (size_t)NCmax * SV;
   size_t budget = (size_t)6 << 30;
   {
     size_t fr = 0, tot = 0;
@@ -1335,20 +1600,8 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     a.dbg_ba = c->dbg;
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
   }
-  const size_t smem = smem_for(P, nt);
-  // two rows per barrier (k_mpdist2): register van Herk, P = 5
-  const size_t smem2 = (size_t)(l + 4 * w + 8 * NCmax + 130) * sizeof(double);
-  // used when one row leaves lane-group slots idle and two rows fit one round
-  bool rows2 = false;
-  if (chm > 0 && P == 5 && smem2 <= smax && nt != 128) {
-    int lpb = 1;
-    while (lpb < 32 && lpb * chm < w) lpb *= 2;
-    if (lpb < 8) lpb = 8;
-    const int64_t slots = (int64_t)(nt / 32) * (32 / lpb);
-    const int64_t nblk = (std::min(T, N) + w - 1) / w;
-    rows2 = 2 * nblk <= slots;
-    if (const char* e = getenv("PASTILA_ROWS2")) rows2 = atoi(e) > 0;  // tuning experiments
-  }
+  const size_t smem = smem_row1(chm == 0, l, w, NCmax, SV);
+  const size_t smem2 = smem_row2(l, w, NCmax, SV);
   // the selection stream starts after everything queued before on the main stream
   PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
   PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[1], 0));
@@ -1360,26 +1613,57 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     a.seg0 = s0;
     a.rowD0 = s0 - seg_lo;
     char* buf = (char*)c->scratch + bi * buf_bytes;
-    a.ab = (double*)buf;
-    a.ba = (double*)(buf + ab_cta * (size_t)ntile * (size_t)segs_per);
+    a.ab = buf;
+    a.ba = buf + ab_cta * (size_t)ntile * (size_t)segs_per;
     dim3 grid((unsigned)ntile, (unsigned)ns);
     PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[bi], 0));  // buffer bi free again
     int r;
-    if (rows2)
-      r = (nt == 512) ? launch_nt2<512>(c, a, grid, chm, smem2) : launch_nt2<256>(c, a, grid, chm, smem2);
+    if (G.rows2)
+      r = (nt == 512) ? launch_nt2<512, V>(c, a, grid, chm, smem2) : launch_nt2<256, V>(c, a, grid, chm, smem2);
     else
-      r = (nt == 512) ? launch_nt<512>(c, a, grid, P, chm, smem)
-          : (nt == 128) ? launch_nt<128>(c, a, grid, P, chm, smem)
-                        : launch_nt<256>(c, a, grid, P, chm, smem);
+      r = (nt == 512) ? launch_nt<512, V>(c, a, grid, P, chm, smem)
+          : (nt == 128) ? launch_nt<128, V>(c, a, grid, P, chm, smem)
+                        : launch_nt<256, V>(c, a, grid, P, chm, smem);
     if (r != PST_OK) return r;
     PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
     PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));
-    r = launch_sel(c, a, grid, (int)NCmax);
+    r = launch_sel<V>(c, a, grid, (int)NCmax);
     if (r != PST_OK) return r;
     PST_CUDA(cudaEventRecord(c->ev_sel[bi], c->st2));
   }
   // the main stream continues only after all selections
   PST_CUDA(cudaEventRecord(c->ev_sel[0], c->st2));
   PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[0], 0));
+  return PST_OK;
+}
+
+int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* seg_dev, const int64_t* win_dev,
+                        int64_t cnt, double* out_dev) {
+  if (cnt <= 0) return PST_OK;
+  PST_TRY(pst_ensure_len(c, l));
+  TileGeom G;
+  PST_TRY(tile_geom(c, m, l, G));
+  const int64_t w = G.w;
+  WinArgs a;
+  a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
+  a.df = c->L.df; a.dg = c->L.dg;
+  a.l = l; a.m = m; a.w = w; a.k = k; a.N = G.N; a.T = G.T;
+  a.seg = seg_dev; a.win = win_dev; a.out = out_dev;
+  const size_t smem = (size_t)(l + 2 * (2 * w - 1) + 3 * w + 2 * (WX_NT / 32) + 2) * sizeof(double);
+  const size_t smax = c->smem_optin ? c->smem_optin : 232448;
+  if (smem > smax) {
+    pst_set_error("window evaluator: snippet size %lld too large", (long long)m);
+    return PST_EINVAL;
+  }
+  if (smem > 48 * 1024) PST_CUDA(cudaFuncSetAttribute(k_window_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int64_t o = 0; o < cnt; o += 65535) {
+    WinArgs b = a;
+    b.seg += o;
+    b.win += o;
+    b.out += o;
+    k_window_exact<<<(unsigned)std::min<int64_t>(65535, cnt - o), WX_NT, smem, c->st>>>(b);
+    c->launches++;
+    PST_CUDA(cudaGetLastError());
+  }
   return PST_OK;
 }

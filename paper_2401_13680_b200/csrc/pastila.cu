@@ -3,6 +3,7 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdarg>
 #include <numeric>
@@ -411,6 +412,221 @@ __global__ void k_gather_rows(const double* __restrict__ D, int64_t ld, const in
     out[r * N + j] = row[j];
 }
 
+// ------------------------------------------------------------ key path
+// The fast profile pass (launch_mpdist_keys) stores, for every (segment,
+// window), the 32-bit key K of the k-th smallest e (high word of its bit
+// pattern).  The exact path's value is d* = f(e*) with f = e_to_dist
+// (monotone) and e* in the bucket [lo(K), hi(K)] (same tiles and fma order:
+// e* is the exact path's own value, not an approximation of it).  Every
+// decision below is taken from monotone interval bounds of d* and is
+// certified; the ones the bounds cannot decide are resolved with exact
+// values (exact profiles of greedy candidates, k_window_exact for single
+// windows), so the outputs equal the all-exact pipeline's bit for bit.
+__device__ __forceinline__ double e2d(double ev, double twol) {  // == e_to_dist (mpdist.cu)
+  if (ev < 1e-15) ev = 0.0;
+  if (ev > 2.0) ev = 2.0;
+  return sqrt(twol * ev);
+}
+// exact interval [f(lo(K)), f(hi(K))]; K < 0 <=> e* < 0 <=> d* = 0
+__host__ __device__ inline double hilo2d(int hi, unsigned lo) {
+  const unsigned long long b = ((unsigned long long)(unsigned)hi << 32) | lo;
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+__device__ __forceinline__ void kb_exact(int K, double twol, double& lo, double& hi) {
+  if (K < 0) {
+    lo = hi = 0.0;
+    return;
+  }
+  lo = e2d(hilo2d(K, 0u), twol);
+  hi = e2d(hilo2d(K, 0xffffffffu), twol);
+}
+constexpr int KEY_TWO = 0x40000000;  // key of e = 2.0 (rho clip): f is constant from here on
+// Cheap outer bounds in fp32 for the greedy area sums: the bucket edges lo(K)
+// and lo(K+1) >= hi(K) are exact floats for 2^-126 <= e <= 2; fp32 product and
+// sqrt errors (<= 3 ulp = 2^-22.4) are covered by the 2^-20 margins.
+// K15 = key of 1e-15 (the snap): below it d* = 0, its bucket straddles it.
+__device__ __forceinline__ void kb_fast(int K, float twolf, int K15, double dclip, double& lo, double& hi) {
+  if (K < K15) {
+    lo = hi = 0.0;
+    return;
+  }
+  if (K >= KEY_TWO) {
+    lo = hi = dclip;
+    return;
+  }
+  const float elo = __int_as_float((K - (896 << 20)) << 3);
+  const float ehi = __int_as_float((K + 1 - (896 << 20)) << 3);
+  lo = (K == K15) ? 0.0 : (double)(__fsqrt_rn(__fmul_rn(twolf, elo)) * (1.0f - 0x1p-20f));
+  hi = (double)(__fsqrt_rn(__fmul_rn(twolf, ehi)) * (1.0f + 0x1p-20f));
+}
+
+// Greedy-step area bounds, same reduction structure as k_areas (per-thread
+// strided fp64 sums + block_sum), so that fp-monotonicity makes
+// alo[s] <= area*[s] <= ahi[s] hold for the rounded sums too.
+__global__ void __launch_bounds__(256) k_areas_kb(const int* __restrict__ Dk, int64_t N, int64_t ld,
+                                                  const double* __restrict__ curve, const uint8_t* __restrict__ taken,
+                                                  float twolf, int K15, double dclip, double* alo, double* ahi) {
+  __shared__ double sh[8];
+  if (taken[blockIdx.x]) {
+    if (threadIdx.x == 0) alo[blockIdx.x] = ahi[blockIdx.x] = PST_INF;
+    return;
+  }
+  const int* row = Dk + blockIdx.x * ld;
+  double al = 0.0, ah = 0.0;
+  for (int64_t j = threadIdx.x; j < N; j += 256) {
+    double lo, hi;
+    kb_fast(row[j], twolf, K15, dclip, lo, hi);
+    if (curve) {
+      const double c = curve[j];
+      lo = fmin(lo, c);
+      hi = fmin(hi, c);
+    }
+    al += lo;
+    ah += hi;
+  }
+  const double tl = block_sum<256>(al, sh);
+  const double th = block_sum<256>(ah, sh);
+  if (threadIdx.x == 0) {
+    alo[blockIdx.x] = tl;
+    ahi[blockIdx.x] = th;
+  }
+}
+
+// greedy candidates: available s with alo[s] <= min over available of ahi
+__global__ void __launch_bounds__(1024) k_greedy_cands(const double* __restrict__ alo, const double* __restrict__ ahi,
+                                                       const uint8_t* __restrict__ taken, int64_t S, int cap,
+                                                       int64_t* list, int* cnt) {
+  __shared__ double wm[32];
+  double m = PST_INF;
+  for (int64_t s = threadIdx.x; s < S; s += blockDim.x)
+    if (!taken[s]) m = fmin(m, ahi[s]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(FULLMASK, m, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = PST_INF;
+  for (int v = 0; v < (int)(blockDim.x >> 5); ++v) m = fmin(m, wm[v]);
+  for (int64_t s = threadIdx.x; s < S; s += blockDim.x)
+    if (!taken[s] && alo[s] <= m) {
+      const int i = atomicAdd(cnt, 1);
+      if (i < cap) list[i] = s;
+    }
+}
+
+// Attribution from keys: per window the smallest key K1, its first segment,
+// its multiplicity and the next larger key K2; certified iff K1 is unique and
+// lo(K2) > hi(K1) (then the first argmin of d* is that segment).  Also the
+// per-window maximum key (profile_max candidates).
+__global__ void k_near_keys(const int* __restrict__ Dk, int64_t S, int64_t N, int64_t ld, double twol,
+                            int32_t* nearest, uint8_t* unc, int* kmaxw, int* K1w) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    int K1 = INT_MAX, K2 = INT_MAX, KM = INT_MIN, n1 = 0;
+    int64_t s1 = 0;
+    for (int64_t s = 0; s < S; ++s) {
+      const int K = Dk[s * ld + j];
+      KM = max(KM, K);
+      if (K < K1) {
+        K2 = K1;
+        K1 = K;
+        s1 = s;
+        n1 = 1;
+      } else if (K == K1) {
+        ++n1;
+      } else {
+        K2 = min(K2, K);
+      }
+    }
+    bool ok = n1 == 1;
+    if (ok && K2 != INT_MAX) {
+      double l1, h1, l2, h2;
+      kb_exact(K1, twol, l1, h1);
+      kb_exact(K2, twol, l2, h2);
+      ok = l2 > h1;
+    }
+    nearest[j] = (int32_t)s1;
+    unc[j] = ok ? 0 : 1;
+    kmaxw[j] = KM;
+    K1w[j] = K1;
+  }
+}
+
+// windows with a flag set -> compact list (unordered)
+__global__ void k_flag_list(const uint8_t* __restrict__ flag, int64_t N, int cap, int64_t* list, int* cnt) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    if (flag[j]) {
+      const int i = atomicAdd(cnt, 1);
+      if (i < cap) list[i] = j;
+    }
+}
+__global__ void k_kmax_flag(const int* __restrict__ kmaxw, int64_t N, int thr, uint8_t* flag) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    flag[j] = kmaxw[j] >= thr ? 1 : 0;
+}
+__global__ void k_max_int(const int* __restrict__ v, int64_t N, int* out) {
+  int m = INT_MIN;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, v[j]);
+  m = __reduce_max_sync(FULLMASK, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// Candidate (segment, window) pairs of listed windows, one warp per window:
+// mode 0 (attribution): segments whose lower bound lo(K) <= hi(K1w[j]);
+// mode 1 (profile_max): segments with K >= thr.
+__global__ void k_pairs(const int* __restrict__ Dk, int64_t S, int64_t ld, const int64_t* __restrict__ wins,
+                        int nwin, const int* __restrict__ K1w, int thr, int mode, double twol, int K15, int cap,
+                        int64_t* pseg, int64_t* pwin, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int wv = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (wv >= nwin) return;
+  const int64_t j = wins[wv];
+  int kthr = thr;
+  if (mode == 0) {  // largest key whose interval can reach below hi(K1)
+    double l1, h1, lo, hi;
+    const int K1 = K1w[j];
+    kb_exact(K1, twol, l1, h1);
+    if (h1 == 0.0) {
+      kthr = K15;  // d* = 0 <=> key < K15, and lo(K15) = 0
+    } else if (K1 >= KEY_TWO) {
+      kthr = INT_MAX;  // f is constant from the clip on
+    } else {
+      kthr = K1;  // adjacent buckets differ by ~2^-21 relative in d: a step or two
+      for (;;) {
+        kb_exact(kthr + 1, twol, lo, hi);
+        if (lo > h1) break;
+        if (kthr + 1 >= KEY_TWO) {
+          kthr = INT_MAX;
+          break;
+        }
+        ++kthr;
+      }
+    }
+  }
+  for (int64_t s = lane; s < S; s += 32) {
+    const int K = Dk[s * ld + j];
+    if (mode == 0 ? K <= kthr : K >= kthr) {
+      const int i = atomicAdd(cnt, 1);
+      if (i < cap) {
+        pseg[i] = s;
+        pwin[i] = j;
+      }
+    }
+  }
+}
+
+__global__ void k_set_nearest(const int64_t* __restrict__ win, const int64_t* __restrict__ seg, int cnt,
+                              int32_t* nearest) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < cnt) nearest[win[i]] = (int32_t)seg[i];
+}
+__global__ void k_mark_taken(uint8_t* taken, int64_t s) { taken[s] = 1; }
+__global__ void k_curve_row(double* curve, const double* __restrict__ row, int64_t N) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
+    curve[j] = fmin(curve[j], row[j]);
+}
+
 int grid_for(int64_t n, int threads, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -517,7 +733,7 @@ int pst_destroy(pst_ctx* c) {
   cudaSetDevice(c->dev);
   cudaStreamSynchronize(c->st);
   void* ptrs[] = {c->x, c->csum, c->csq, c->chg, c->L.mu, c->L.var, c->L.sd, c->L.nrm, c->L.bias,
-                  c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg};
+                  c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg, c->Dk, c->cert};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st2) {
@@ -758,6 +974,24 @@ int pst_profile_reduce_dev(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t 
   return PST_OK;
 }
 
+static int run_select_keys(pst_ctx* c, const int* Dk, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N,
+                           int64_t n, int64_t K, pst_snippets* res);
+
+// Key path (launch_mpdist_keys + certified selection) when the S x N key matrix
+// fits next to the profile-kernel scratch; PASTILA_EXACT=1 forces the exact
+// path (A/B and parity tests), PASTILA_STREAM_ROWS the streamed exact path.
+static bool use_keys(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
+  if (const char* e = getenv("PASTILA_EXACT"))
+    if (atoi(e) > 0) return false;
+  if (getenv("PASTILA_STREAM_ROWS")) return false;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+  const size_t have = fr + c->Dk_bytes + c->D_bytes;
+  const size_t seg_scratch = (size_t)N * 4 * (size_t)(w + w / 10 + 2);
+  const size_t reserve = std::max((size_t)8 << 30, 2 * seg_scratch) + (size_t)N * 8 * (24 + 16) + ((size_t)3 << 30);
+  return have > reserve && (size_t)S * N * sizeof(int) <= have - reserve;
+}
+
 int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res) {
   if (!valid(c)) return PST_EINVAL;
   PST_CUDA(cudaSetDevice(c->dev));
@@ -771,6 +1005,23 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
   if (K < 1 || K > S) {
     pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
     return PST_EINVAL;
+  }
+  if (use_keys(c, S, N, m - l + 1)) {
+    if (c->D) {  // the exact matrix is not needed on this path
+      cudaFree(c->D);
+      c->D = nullptr;
+      c->D_bytes = 0;
+    }
+    PST_TRY(pst_ensure((void**)&c->Dk, &c->Dk_bytes, (size_t)S * N * sizeof(int)));
+    PST_TRY(launch_mpdist_keys(c, m, l, k, 0, S, c->Dk, N));
+    const int r = run_select_keys(c, c->Dk, m, l, k, S, N, n, K, res);
+    if (r != 1) return r;
+    c->cert_stats[6]++;  // a certification cap was exceeded: recompute this length exactly
+  }
+  if (c->Dk) {
+    cudaFree(c->Dk);
+    c->Dk = nullptr;
+    c->Dk_bytes = 0;
   }
   const int64_t chunk = profile_chunk_rows(c, S, N, m - l + 1);
   if (chunk < S) return run_select_streamed(c, m, l, k, S, N, n, K, chunk, res);
@@ -1023,6 +1274,241 @@ static int run_select_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int6
   return finish_select(c, b, S, N, n, K, b.rows, steps, res);
 }
 
+// ---------------------------------------------------------------- key path
+static double e2d_h(double ev, double twol) {  // host twin of e2d / e_to_dist (IEEE ops, same order)
+  if (ev < 1e-15) ev = 0.0;
+  if (ev > 2.0) ev = 2.0;
+  return sqrt(twol * ev);
+}
+static void kb_exact_h(int K, double twol, double& lo, double& hi) {
+  if (K < 0) {
+    lo = hi = 0.0;
+    return;
+  }
+  lo = e2d_h(hilo2d(K, 0u), twol);
+  hi = e2d_h(hilo2d(K, 0xffffffffu), twol);
+}
+
+// caps of the exact work one key-path selection may need; beyond them the
+// length is recomputed on the exact path (degenerate inputs: many exact ties)
+constexpr int CAP_G = 16;        // exact greedy candidates per step
+constexpr int CAP_W = 1 << 16;   // uncertain attribution / max windows
+constexpr int CAP_P = 1 << 18;   // exact (segment, window) evaluations
+
+struct CertBufs {
+  double *alo, *ahi, *crow, *carea, *pval;
+  int64_t *glist, *wins, *pseg, *pwin;
+  int *cnt, *kmaxw, *K1w;
+  uint8_t* unc;
+};
+static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t o_alo = take(S * 8), o_ahi = take(S * 8), o_crow = take((size_t)CAP_G * N * 8),
+               o_carea = take(CAP_G * 8), o_pval = take((size_t)CAP_P * 8), o_gl = take(CAP_G * 8),
+               o_w = take((size_t)CAP_W * 8), o_ps = take((size_t)CAP_P * 8), o_pw = take((size_t)CAP_P * 8),
+               o_cnt = take(4 * 4), o_km = take(N * 4), o_k1 = take(N * 4), o_unc = take(N);
+  PST_TRY(pst_ensure(&c->cert, &c->cert_bytes, off));
+  char* p = (char*)c->cert;
+  b.alo = (double*)(p + o_alo);
+  b.ahi = (double*)(p + o_ahi);
+  b.crow = (double*)(p + o_crow);
+  b.carea = (double*)(p + o_carea);
+  b.pval = (double*)(p + o_pval);
+  b.glist = (int64_t*)(p + o_gl);
+  b.wins = (int64_t*)(p + o_w);
+  b.pseg = (int64_t*)(p + o_ps);
+  b.pwin = (int64_t*)(p + o_pw);
+  b.cnt = (int*)(p + o_cnt);
+  b.kmaxw = (int*)(p + o_km);
+  b.K1w = (int*)(p + o_k1);
+  b.unc = (uint8_t*)(p + o_unc);
+  return PST_OK;
+}
+
+// exact values of the listed (segment, window) pairs -> host vectors
+static int eval_pairs(pst_ctx* c, int64_t m, int64_t l, int64_t k, CertBufs& cb, int cnt, std::vector<int64_t>& seg,
+                      std::vector<int64_t>& win, std::vector<double>& val) {
+  seg.resize(cnt);
+  win.resize(cnt);
+  val.resize(cnt);
+  if (cnt == 0) return PST_OK;
+  PST_TRY(launch_window_exact(c, m, l, k, cb.pseg, cb.pwin, cnt, cb.pval));
+  PST_CUDA(cudaMemcpyAsync(seg.data(), cb.pseg, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(win.data(), cb.pwin, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(val.data(), cb.pval, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  c->cert_stats[4] += cnt;
+  return PST_OK;
+}
+
+static int read_cnt(pst_ctx* c, const int* dcnt, int& h) {
+  PST_CUDA(cudaMemcpyAsync(&h, dcnt, 4, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// Greedy + attribution + profile_max on the resident key matrix Dk (S x N).
+// Returns PST_OK, or 1 when a cap is exceeded (caller falls back to the exact path).
+static int run_select_keys(pst_ctx* c, const int* Dk, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N,
+                           int64_t n, int64_t K, pst_snippets* res) {
+  const double twol = 2.0 * (double)l;
+  const float twolf = (float)twol;
+  int K15;
+  {
+    const double t = 1e-15;
+    unsigned long long bits;
+    memcpy(&bits, &t, 8);
+    K15 = (int)(bits >> 32);
+  }
+  const double dclip = e2d_h(2.0, twol);
+  SelBufs b;
+  PST_TRY(sel_bufs(c, S, N, n, K, true, b));  // rows: the K chosen exact profiles
+  CertBufs cb;
+  PST_TRY(cert_bufs(c, S, N, cb));
+  c->cert_stats[0]++;
+  c->cert_stats[7] += N;
+
+  // ---- greedy (snippets.py:201-210)
+  PST_CUDA(cudaMemsetAsync(b.taken, 0, S, c->st));
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, HUGE_VAL, N);
+  c->launches++;
+  std::vector<int64_t> chosen(K);
+  for (int64_t step = 0; step < K; ++step) {
+    const double* cur = step == 0 ? nullptr : b.curve;
+    k_areas_kb<<<(unsigned)S, 256, 0, c->st>>>(Dk, N, N, cur, b.taken, twolf, K15, dclip, cb.alo, cb.ahi);
+    PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 4, c->st));
+    k_greedy_cands<<<1, 1024, 0, c->st>>>(cb.alo, cb.ahi, b.taken, S, CAP_G, cb.glist, cb.cnt);
+    c->launches += 2;
+    PST_CUDA(cudaGetLastError());
+    int nc = 0;
+    PST_TRY(read_cnt(c, cb.cnt, nc));
+    if (nc > CAP_G || nc < 1) return 1;
+    std::vector<int64_t> cand(nc);
+    PST_CUDA(cudaMemcpyAsync(cand.data(), cb.glist, (size_t)nc * 8, cudaMemcpyDeviceToHost, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));
+    std::sort(cand.begin(), cand.end());
+    c->cert_stats[1] += nc;
+    if (nc > 1) c->cert_stats[2]++;
+    for (int i = 0; i < nc; ++i) {  // exact profiles and exact areas (k_areas, as the exact path)
+      double* row = cb.crow + (size_t)i * N;
+      PST_TRY(launch_mpdist(c, m, l, k, cand[i], cand[i] + 1, row, N));
+      k_areas<<<1, 256, 0, c->st>>>(row, N, N, cur, cb.carea + i);
+      c->launches++;
+    }
+    std::vector<double> ca(nc);
+    PST_CUDA(cudaMemcpyAsync(ca.data(), cb.carea, (size_t)nc * 8, cudaMemcpyDeviceToHost, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));
+    int bi = 0;
+    for (int i = 1; i < nc; ++i)
+      if (ca[i] < ca[bi]) bi = i;  // ties -> lowest index (cand sorted)
+    chosen[step] = cand[bi];
+    double* keep = b.rows + step * N;
+    PST_CUDA(cudaMemcpyAsync(keep, cb.crow + (size_t)bi * N, (size_t)N * 8, cudaMemcpyDeviceToDevice, c->st));
+    k_mark_taken<<<1, 1, 0, c->st>>>(b.taken, cand[bi]);
+    k_curve_row<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, keep, N);
+    c->launches += 2;
+  }
+  PST_CUDA(cudaMemcpyAsync(b.best, chosen.data(), K * 8, cudaMemcpyHostToDevice, c->st));
+
+  // ---- attribution (snippets.py:212-213) and profile_max (snippets.py:241)
+  k_near_keys<<<grid_for(N, 256), 256, 0, c->st>>>(Dk, S, N, N, twol, b.nearest, cb.unc, cb.kmaxw, cb.K1w);
+  PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 16, c->st));
+  k_flag_list<<<grid_for(N, 256), 256, 0, c->st>>>(cb.unc, N, CAP_W, cb.wins, cb.cnt);
+  c->launches += 2;
+  PST_CUDA(cudaGetLastError());
+  int nw = 0;
+  PST_TRY(read_cnt(c, cb.cnt, nw));
+  if (nw > CAP_W) return 1;
+  c->cert_stats[3] += nw;
+  std::vector<int64_t> ps, pw;
+  std::vector<double> pv;
+  if (nw > 0) {
+    k_pairs<<<(unsigned)((nw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, cb.wins, nw, cb.K1w, 0, 0, twol, K15, CAP_P,
+                                                                cb.pseg, cb.pwin, cb.cnt + 1);
+    c->launches++;
+    int np = 0;
+    PST_TRY(read_cnt(c, cb.cnt + 1, np));
+    if (np > CAP_P) return 1;
+    PST_TRY(eval_pairs(c, m, l, k, cb, np, ps, pw, pv));
+    // per window: first argmin of the exact values
+    std::vector<size_t> ord(np);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t bb) {
+      if (pw[a] != pw[bb]) return pw[a] < pw[bb];
+      if (pv[a] != pv[bb]) return pv[a] < pv[bb];
+      return ps[a] < ps[bb];
+    });
+    std::vector<int64_t> fw, fs;
+    for (size_t i = 0; i < ord.size(); ++i)
+      if (i == 0 || pw[ord[i]] != pw[ord[i - 1]]) {
+        fw.push_back(pw[ord[i]]);
+        fs.push_back(ps[ord[i]]);
+      }
+    const int nf = (int)fw.size();
+    if (nf > 0) {
+      PST_CUDA(cudaMemcpyAsync(cb.wins, fw.data(), (size_t)nf * 8, cudaMemcpyHostToDevice, c->st));
+      PST_CUDA(cudaMemcpyAsync(cb.pseg, fs.data(), (size_t)nf * 8, cudaMemcpyHostToDevice, c->st));
+      k_set_nearest<<<(nf + 255) / 256, 256, 0, c->st>>>(cb.wins, cb.pseg, nf, b.nearest);
+      c->launches++;
+    }
+  }
+  double pmax = 0.0;
+  {
+    static const int kIntMin = INT_MIN;
+    PST_CUDA(cudaMemcpyAsync(cb.cnt + 2, &kIntMin, 4, cudaMemcpyHostToDevice, c->st));
+    k_max_int<<<grid_for(N, 256, 1024), 256, 0, c->st>>>(cb.kmaxw, N, cb.cnt + 2);
+    c->launches++;
+    int kmax = 0;
+    PST_TRY(read_cnt(c, cb.cnt + 2, kmax));
+    double lo, hi;
+    kb_exact_h(kmax, twol, lo, hi);
+    if (lo == hi) {
+      pmax = lo;
+    } else {  // candidates: every (segment, window) whose interval reaches lo(kmax)
+      // keys below K15 are exactly 0 and cannot exceed a candidate; adjacent
+      // buckets differ by ~2^-21 relative, so the loop takes a step or two
+      int thr = kmax, guard = 0;
+      while (thr > K15) {
+        double l2, h2;
+        kb_exact_h(thr - 1, twol, l2, h2);
+        if (h2 < lo) break;
+        --thr;
+        if (++guard > 1024) return 1;
+      }
+      k_kmax_flag<<<grid_for(N, 256), 256, 0, c->st>>>(cb.kmaxw, N, thr, cb.unc);
+      PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 8, c->st));
+      k_flag_list<<<grid_for(N, 256), 256, 0, c->st>>>(cb.unc, N, CAP_W, cb.wins, cb.cnt);
+      c->launches += 2;
+      int nmw = 0;
+      PST_TRY(read_cnt(c, cb.cnt, nmw));
+      if (nmw > CAP_W || nmw < 1) return 1;
+      k_pairs<<<(unsigned)((nmw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, cb.wins, nmw, cb.K1w, thr, 1, twol,
+                                                                   K15, CAP_P, cb.pseg, cb.pwin, cb.cnt + 1);
+      c->launches++;
+      int np = 0;
+      PST_TRY(read_cnt(c, cb.cnt + 1, np));
+      if (np > CAP_P || np < 1) return 1;
+      PST_TRY(eval_pairs(c, m, l, k, cb, np, ps, pw, pv));
+      c->cert_stats[5] += np;
+      for (double v : pv) pmax = std::max(pmax, v);
+    }
+  }
+  {
+    unsigned long long bits;
+    memcpy(&bits, &pmax, 8);
+    PST_CUDA(cudaMemcpyAsync(b.dmax, &bits, 8, cudaMemcpyHostToDevice, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));  // &bits is a stack variable
+  }
+  std::vector<int64_t> steps(K);
+  std::iota(steps.begin(), steps.end(), 0);
+  return finish_select(c, b, S, N, n, K, b.rows, steps, res);
+}
+
 // criterion_score on caller-supplied profiles (length_select.py:56-87):
 // P host [K*N] in snippet order, pairs summed in itertools.combinations order.
 int pst_criterion(pst_ctx* c, const double* P, int64_t K, int64_t N, double profile_max, double* out) {
@@ -1071,6 +1557,64 @@ int pst_labels(pst_ctx* c, const double* P, int64_t K, int64_t N, int64_t n, int
   c->launches++;
   PST_CUDA(cudaGetLastError());
   PST_CUDA(cudaMemcpyAsync(labels, dl, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// Certification counters of the key path (see pst_ctx::cert_stats); reset != 0 clears them.
+int pst_cert_stats(pst_ctx* c, int64_t* out, int reset) {
+  if (!valid(c)) return PST_EINVAL;
+  if (out)
+    for (int i = 0; i < 8; ++i) out[i] = c->cert_stats[i];
+  if (reset)
+    for (int i = 0; i < 8; ++i) c->cert_stats[i] = 0;
+  return PST_OK;
+}
+
+// Key-path profile keys of segments [seg_lo, seg_hi) (host out [(hi-lo) * N]):
+// out = high word of the exact path's e_k (test / certification evidence).
+int pst_profile_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, int32_t* out) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t S = c->n / m, N = c->n - m + 1;
+  if (seg_lo < 0 || seg_hi > S || seg_lo >= seg_hi) {
+    pst_set_error("segment index %lld out of range [0, %lld)", (long long)(seg_lo < 0 ? seg_lo : seg_hi - 1),
+                  (long long)S);
+    return PST_EINVAL;
+  }
+  const size_t bytes = (size_t)(seg_hi - seg_lo) * N * sizeof(int);
+  PST_TRY(pst_ensure((void**)&c->Dk, &c->Dk_bytes, bytes));
+  PST_TRY(launch_mpdist_keys(c, m, l, k, seg_lo, seg_hi, c->Dk, N));
+  PST_CUDA(cudaMemcpyAsync(out, c->Dk, bytes, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// Exact profile values at single (segment, window) pairs (host arrays of cnt).
+int pst_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* seg, const int64_t* win,
+                     int64_t cnt, double* out) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaSetDevice(c->dev));
+  PST_TRY(check_mkl(c, m, l, k));
+  const int64_t S = c->n / m, N = c->n - m + 1;
+  for (int64_t i = 0; i < cnt; ++i)
+    if (seg[i] < 0 || seg[i] >= S || win[i] < 0 || win[i] >= N) {
+      pst_set_error("pair %lld (segment %lld, window %lld) out of range", (long long)i, (long long)seg[i],
+                    (long long)win[i]);
+      return PST_EINVAL;
+    }
+  if (cnt <= 0) return PST_OK;
+  const size_t b = (size_t)cnt * 8;
+  PST_TRY(pst_ensure(&c->work, &c->work_bytes, 3 * ((b + 255) & ~(size_t)255)));
+  char* w = (char*)c->work;
+  int64_t* ds = (int64_t*)w;
+  int64_t* dw = (int64_t*)(w + ((b + 255) & ~(size_t)255));
+  double* dv = (double*)(w + 2 * ((b + 255) & ~(size_t)255));
+  PST_CUDA(cudaMemcpyAsync(ds, seg, b, cudaMemcpyHostToDevice, c->st));
+  PST_CUDA(cudaMemcpyAsync(dw, win, b, cudaMemcpyHostToDevice, c->st));
+  PST_TRY(launch_window_exact(c, m, l, k, ds, dw, cnt, dv));
+  PST_CUDA(cudaMemcpyAsync(out, dv, b, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
   return PST_OK;
 }

@@ -121,6 +121,7 @@ struct TileGeom {
   int64_t w, N, NCmax, T, ntile, R, Tp;
   int nt, P, chm;
   bool rows2;
+  bool v2;         // k_rowsP (thread-owned windows) instead of k_mpdist / k_mpdist2
   size_t smem_d;   // dynamic smem of the one-row kernel with V = double (geometry decisions)
 };
 int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& g);

@@ -943,6 +943,245 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   }
 }
 
+// ---- row loop, thread-owned windows (w - 1 divisible by P) ------------------
+// Deterministic sum of xs[0..l) by one warp: lane-strided partial sums, an
+// xor tree, lane 0's result broadcast (the same procedure in k_window_exact).
+__device__ __forceinline__ double warp_sum_fixed(const double* xs, int l, int lane) {
+  double s = 0.0;
+  for (int t = lane; t < l; t += 32) s += xs[t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULLMASK, s, o);
+  return __shfl_sync(FULLMASK, s, 0);
+}
+
+// Thread t owns columns [tP, tP+P) of the tile and windows [tP, tP+P).  With
+// w - 1 = D*P, window tP+u ends at column (t+D)P + u, so its row minimum is
+//   AB = min(SUF_t[u], MID_t, PRE_{t+D}[u]),  MID_t = min(bm[t+1 .. t+D-1]),
+// where SUF/PRE are the thread-local suffix/prefix minima of a thread's P
+// keys and bm its block minimum: 2 minima per key in registers, one 3-way
+// minimum per window, vector shared-memory stores/loads of the PRE blocks, and
+// the D-1 block minima (level 2) from shared memory -- read directly for
+// D-1 <= 8, else through minima of 8 consecutive blocks (G).  No cross-lane
+// scans.  AB rows go straight to the lane-run scratch layout of k_select_run.
+// e values: same per-cell arithmetic as k_mpdist (row-0 and left-edge fresh
+// dots in the same per-column fma order, same recurrence and e formula); the
+// centered-window sums use warp_sum_fixed.
+template <int P, int NT, class V>
+__global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NCmax = NT * P;
+  const int l = (int)a.l, w = (int)a.w;
+  const int D = (w - 1) / P, L2 = D - 1;
+  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t J0 = (int64_t)blockIdx.x * a.T;
+  const int NJ = (int)min(a.T, a.N - J0);
+  const int NC = NJ + w - 1;
+  double* xs = (double*)smraw;  // [l]
+  double* edge = xs + l;        // [w]
+  double* rdf = edge + w;       // [w]
+  double* rdg = rdf + w;        // [w]
+  double* rnq = rdg + w;        // [w]
+  double* xfer = rnq + w;       // [2][32]
+  double* red = xfer + 64;      // [2]
+  constexpr int PS = P + 1;  // per-thread stride of the prefix-minima rows (odd: conflict-free)
+  V* PREB = (V*)(smraw + align16((size_t)(l + 4 * w + 66) * 8));  // [2][NT*PS + 8*PS] prefix minima by row parity
+  V* BMB = PREB + 2 * (NT * PS + 8 * PS);                          // [2][NT + 40] block minima
+  V* GB = BMB + 2 * (NT + 40);                                     // [NT + 40] minima of 8 blocks
+  V* BAs = GB;                                                     // allP_BA staging at the end (reuses GB..)
+  const int R = (int)a.R, Tp = (int)a.Tp;
+  V* ab = (V*)a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
+  const double* __restrict__ xJ = a.x + J0;
+  const double* __restrict__ xQ = a.x + q0;
+  const double* __restrict__ muJ = a.mu + J0;
+  const double* __restrict__ muQ = a.mu + q0;
+  const int c0 = tid * P;
+
+  // ---- row-0 fresh dots (register-blocked: x window slides through registers)
+  {
+    const double mq = muQ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xQ[t] - mq;
+    __syncthreads();
+    if (warp == 0) {
+      const double s1 = warp_sum_fixed(xs, l, lane);
+      if (lane == 0) red[0] = s1;
+    }
+    __syncthreads();
+  }
+  double cov[P];
+  {
+    const double sx = red[0];
+    double xw[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      cov[p] = 0.0;
+      xw[p] = (c0 + p < NC + l - 1) ? xJ[c0 + p] : 0.0;  // samples (not columns) of the window
+    }
+#pragma unroll 4
+    for (int t = 0; t < l; ++t) {
+      const double xt = xs[t];
+#pragma unroll
+      for (int p = 0; p < P; ++p) cov[p] = fma(xt, xw[p], cov[p]);
+#pragma unroll
+      for (int p = 0; p < P - 1; ++p) xw[p] = xw[p + 1];
+      xw[P - 1] = (c0 + P + t < NC + l - 1) ? xJ[c0 + P + t] : 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) cov[p] = (c0 + p < NC) ? fma(-muJ[c0 + p], sx, cov[p]) : 0.0;
+  }
+  __syncthreads();
+  // ---- left edge (column J0) for rows 1..w-1
+  {
+    const double mc = muJ[0];
+    for (int t = tid; t < l; t += NT) xs[t] = xJ[t] - mc;
+    __syncthreads();
+    if (warp == 0) {
+      const double s1 = warp_sum_fixed(xs, l, lane);
+      if (lane == 0) red[1] = s1;
+    }
+    __syncthreads();
+    const double sx = red[1];
+    for (int i = 1 + tid; i < w; i += NT) {
+      const double* xq = xQ + i;
+      double acc = 0.0;
+      for (int t = 0; t < l; ++t) acc = fma(xq[t], xs[t], acc);
+      edge[i] = fma(-muQ[i], sx, acc);
+    }
+  }
+  for (int i = tid; i < w; i += NT) {
+    rdf[i] = i > 0 ? a.df[q0 + i - 1] : 0.0;
+    rdg[i] = i > 0 ? a.dg[q0 + i - 1] : 0.0;
+    rnq[i] = a.nrm[q0 + i];
+  }
+  double dgc[P], dfc[P], nrmc[P];
+  V colmin[P];
+  double bic[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int cl = c0 + p;
+    const bool ok = cl < NC;
+    const int64_t c = J0 + cl;
+    dgc[p] = (ok && c > 0) ? a.dg[c - 1] : 0.0;
+    dfc[p] = (ok && c > 0) ? a.df[c - 1] : 0.0;
+    nrmc[p] = ok ? a.nrm[c] : 0.0;
+    bic[p] = ok ? a.bias[c] : 1.0;
+    colmin[p] = VT<V>::inf();
+  }
+  bool cst = false;  // a constant column (bias 0.5) among mine
+#pragma unroll
+  for (int p = 0; p < P; ++p) cst |= bic[p] != 1.0 && c0 + p < NC;
+  const bool cst_tile = __syncthreads_or(cst);  // rare: constant windows in the tile
+  const bool tail = c0 + P > NC;
+  const bool self_tile = (q0 + w > J0) && (q0 < J0 + NC);
+  const int qloc = (int)(q0 - J0) - c0;
+  // lane-run scratch positions of my windows (window j -> (j % R) * 32 + j / R)
+  int pos[P];
+  const int nwok = min(P, max(0, NJ - c0));  // my valid windows
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int j = c0 + p;
+    pos[p] = (j % R) * 32 + j / R;
+  }
+  const bool rem_ok = tid + D < NT;  // my windows' last columns exist in this tile
+  __syncthreads();
+
+  for (int i = 0; i < w; ++i) {
+    const int par = i & 1;
+    double left = __shfl_up_sync(FULLMASK, cov[P - 1], 1);
+    if (i > 0) {
+      const double dfq = rdf[i], dgq = rdg[i];
+      if (lane == 0 && warp > 0) left = xfer[((i - 1) & 1) * 32 + warp - 1];
+#pragma unroll
+      for (int p = P - 1; p >= 1; --p) cov[p] = fma(dfq, dgc[p], fma(dgq, dfc[p], cov[p - 1]));
+      cov[0] = (tid == 0) ? edge[i] : fma(dfq, dgc[0], fma(dgq, dfc[0], left));
+    }
+    if (lane == 31) xfer[par * 32 + warp] = cov[P - 1];
+    const double nq = rnq[i];
+    V kk[P];
+    if (nq != 0.0) {
+      const double mnq = -nq;
+      if (!cst_tile) {  // every column non-constant: bias 1.0
+#pragma unroll
+        for (int p = 0; p < P; ++p) kk[p] = VT<V>::of(fma(cov[p] * mnq, nrmc[p], 1.0));
+      } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+          kk[p] = VT<V>::of(fma(cov[p] * mnq, nrmc[p], (c0 + p < NC) ? a.bias[J0 + c0 + p] : PST_INF));
+      }
+    } else {  // constant query window (row-uniform branch): zdist.py:111-112
+#pragma unroll
+      for (int p = 0; p < P; ++p) kk[p] = (c0 + p < NC) ? VT<V>::of(a.cbias[J0 + c0 + p]) : VT<V>::inf();
+    }
+    if (tail) {
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (c0 + p >= NC) kk[p] = VT<V>::inf();
+    }
+    if (self_tile) {  // self column (zdist.py:121-122)
+      const int ql = qloc + i;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (ql == p) kk[p] = VT<V>::of(0.0);
+    }
+    V sf[P], pr[P];
+    sf[P - 1] = kk[P - 1];
+#pragma unroll
+    for (int p = P - 2; p >= 0; --p) sf[p] = vmin(kk[p], sf[p + 1]);
+    pr[0] = kk[0];
+#pragma unroll
+    for (int p = 1; p < P; ++p) pr[p] = vmin(pr[p - 1], kk[p]);
+#pragma unroll
+    for (int p = 0; p < P; ++p) colmin[p] = vmin(colmin[p], kk[p]);
+    V* PRE = PREB + par * (NT * PS + 8 * PS);
+    V* BM = BMB + par * (NT + 40);
+#pragma unroll
+    for (int p = 0; p < P; ++p) PRE[tid * PS + p] = pr[p];
+    BM[tid] = sf[0];
+    __syncthreads();
+    V mid = VT<V>::inf();
+    if (L2 <= 8) {
+      for (int d = 1; d <= L2; ++d) mid = vmin(mid, BM[tid + d]);
+    } else {
+      V g = BM[tid];
+#pragma unroll
+      for (int d = 1; d < 8; ++d) g = vmin(g, BM[min(tid + d, NT - 1)]);
+      GB[tid] = g;
+      __syncthreads();
+      int d = 1;
+      for (; d + 8 <= L2; d += 8) mid = vmin(mid, GB[min(tid + d, NT - 1)]);
+      mid = vmin(mid, GB[min(tid + L2 - 7, NT - 1)]);
+    }
+    if (rem_ok) {
+      const V* rp = PRE + (tid + D) * PS;
+      V* abrow = ab + (int64_t)i * Tp;
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p < nwok) abrow[pos[p]] = vmin(vmin(sf[p], mid), rp[p]);
+    }
+  }
+  // ---- allP_BA (column minima); self columns [q0, q0+w) are exactly 0
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int cl = c0 + p;
+    const int64_t c = J0 + cl;
+    if (cl < NC) BAs[cl] = (c >= q0 && c < q0 + w) ? VT<V>::of(0.0) : colmin[p];
+  }
+  __syncthreads();
+  {
+    V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
+    for (int c = tid; c < NC; c += NT) bag[c] = BAs[c];
+    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+      for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = BAs[c];
+  }
+}
+__host__ __device__ inline size_t smem_rowsP(int64_t l, int64_t w, int NT, int P, size_t sv) {
+  // doubles, then PREB [2][NCmax + 8P], BMB [2][NT + 40], GB / BA staging [max(NT + 40, NCmax)]
+  const size_t ncm = (size_t)NT * P;
+  return align16((size_t)(l + 4 * w + 66) * 8) + (2 * ((size_t)NT * (P + 1) + 8 * (P + 1)) + 2 * (NT + 40) +
+                                                 std::max((size_t)NT + 40, ncm)) * sv;
+}
+
 // Generic (memory-resident) variant of the warp selection for 2w > 32*2*16.
 template <class V>
 struct MemWin {
@@ -1099,7 +1338,23 @@ __device__ __forceinline__ V solve_window(const V* __restrict__ ab, const V* BA,
   return x;
 }
 
-template <int NWS, int TM, class V>
+// Lane pass of one window: counts of the pivot p and the two nearest values
+// on each side of it (multisets: duplicates kept), so that rank moves of one
+// or two resolve without the warp-cooperative solve.
+template <class V>
+__device__ __forceinline__ void lane_acc(V v, V p, int& lt, int& le, V& b1, V& b2, V& a1, V& a2) {
+  const bool l = v < p, e = v <= p;
+  lt += l;
+  le += e;
+  const V vb = l ? v : VT<V>::ninf();
+  const V va = e ? VT<V>::inf() : v;
+  b2 = vmax(b2, vmin(b1, vb));
+  b1 = vmax(b1, vb);
+  a2 = vmin(a2, vmax(a1, va));
+  a1 = vmin(a1, va);
+}
+
+template <int NWS, int TM, class V, bool LP>
 __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int NCmax) {
   using O = typename OutT<V>::type;
   extern __shared__ __align__(16) unsigned char smsel[];
@@ -1155,6 +1410,51 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
     }
     if (jl + r0 < NJ) put_out(Drow, jl + r0, p, twol);
   }
+  if constexpr (LP) {
+    // every window: one lane-local pass over its 2w values (A from the scratch,
+    // B from shared memory); only rank moves beyond 2 go to the warp
+    for (int r = r0 + 1; r < r1; ++r) {
+      const int j = jl + r;
+      const bool ok = j < NJ;
+      const V* Ap = ab + r * 32 + lane;
+      const V* Bp = BA + (ok ? j : 0);
+      int lt = 0, le = 0;
+      V b1 = VT<V>::ninf(), b2 = VT<V>::ninf(), a1 = VT<V>::inf(), a2 = VT<V>::inf();
+      constexpr int kUn = TM >= 7 || TM == 0 ? 16 : 8;
+#pragma unroll kUn
+      for (int i = 0; i < w; ++i) {
+        lane_acc<V>(__ldg(Ap + (int64_t)i * Tp), p, lt, le, b1, b2, a1, a2);
+        lane_acc<V>(Bp[i], p, lt, le, b1, b2, a1, a2);
+      }
+      V ans = p;
+      bool done = lt < k && k <= le;
+      if (!done) {
+        if (k <= lt) {
+          const int need = lt - k + 1;  // rank from the top among the values below p
+          if (need == 1) { ans = b1; done = true; }
+          else if (need == 2) { ans = b2; done = true; }
+        } else {
+          const int need = k - le;  // rank among the values above p
+          if (need == 1) { ans = a1; done = true; }
+          else if (need == 2) { ans = a2; done = true; }
+        }
+      }
+      unsigned pend = __ballot_sync(FULLMASK, ok && !done);
+      if (a.dbg_flags & 1) pend = 0;
+      while (pend) {
+        const int L = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const V pl = __shfl_sync(FULLMASK, p, L);
+        const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
+        int b1c, b2c;
+        const V x = solve_window<TM, V>(ab, BA, w, k, R, Tp, L, r, lane, false, pl, ltl, lel, b1c, b2c, colbuf);
+        if (lane == L) ans = x;
+      }
+      p = ans;
+      if (ok) put_out(Drow, j, p, twol);
+    }
+    return;
+  }
   for (int r = r0 + 1; r < r1; ++r) {
     const int j = jl + r;
     const bool ok = j < NJ;
@@ -1205,6 +1505,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
 struct WinArgs {
   const double *x, *mu, *nrm, *bias, *cbias, *df, *dg;
   int64_t l, m, w, k, N, T;
+  int sumfixed;  // 1: centered-window sums by warp_sum_fixed (k_rowsP tiles), 0: sequential (k_mpdist)
   const int64_t *seg, *win;
   double* out;
 };
@@ -1233,7 +1534,12 @@ __global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
     const double mq = a.mu[q0];
     for (int t = tid; t < l; t += WX_NT) xs[t] = xQ[t] - mq;
     __syncthreads();
-    if (tid == 0) {
+    if (a.sumfixed) {
+      if (warp == 0) {
+        const double s1 = warp_sum_fixed(xs, l, lane);
+        if (lane == 0) red[0] = s1;
+      }
+    } else if (tid == 0) {
       double s1 = 0.0;
       for (int t = 0; t < l; ++t) s1 += xs[t];
       red[0] = s1;
@@ -1253,7 +1559,12 @@ __global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
     const double mc = a.mu[J0];
     for (int t = tid; t < l; t += WX_NT) xs[t] = xJ[t] - mc;
     __syncthreads();
-    if (tid == 0) {
+    if (a.sumfixed) {
+      if (warp == 0) {
+        const double s1 = warp_sum_fixed(xs, l, lane);
+        if (lane == 0) red[1] = s1;
+      }
+    } else if (tid == 0) {
       double s1 = 0.0;
       for (int t = 0; t < l; ++t) s1 += xs[t];
       red[1] = s1;
@@ -1343,7 +1654,9 @@ int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
 template <int NWS, int TM, class V>
 int launch_sel_w(pst_ctx* c, const MPArgs& a, dim3 grid, int NCmax) {
   const size_t smem = (size_t)(NCmax + (TM == 0 ? NWS * a.w : 0)) * sizeof(V);
-  auto kern = k_select_run<NWS, TM, V>;
+  // lane-pass selection (default) or count pass + warp solves (PASTILA_SEL=0, A/B)
+  static const bool lp = !(getenv("PASTILA_SEL") && atoi(getenv("PASTILA_SEL")) == 0);
+  auto kern = lp ? k_select_run<NWS, TM, V, true> : k_select_run<NWS, TM, V, false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -1426,6 +1739,20 @@ int launch_nt(pst_ctx* c, const MPArgs& a, dim3 grid, int P, int chm, size_t sme
   }
 }
 
+template <int P, class V>
+int launch_rowsP(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
+  auto kern = k_rowsP<P, 256, V>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PST_ECUDA;
+  }
+  kern<<<grid, 256, smem, c->st>>>(a);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
 }  // namespace
 
 // Tile geometry (measured rules).  Decisions use the
@@ -1435,6 +1762,27 @@ int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& G) {
   const int64_t n = c->n, w = m - l + 1, N = n - m + 1;
   G.w = w;
   G.N = N;
+  G.v2 = false;
+  {  // thread-owned windows (k_rowsP): w - 1 divisible by P = 8 or 4, 256 threads
+    const char* e = getenv("PASTILA_V2");  // opt-in (experiment): slower than k_mpdist so far
+    const bool allow = e && atoi(e) > 0;
+    const int P2 = ((w - 1) % 8 == 0) ? 8 : ((w - 1) % 4 == 0) ? 4 : 0;
+    if (allow && P2 && w >= P2 + 1 && w <= 289) {
+      G.v2 = true;
+      G.nt = 256;
+      G.P = P2;
+      G.chm = 0;
+      G.rows2 = false;
+      G.NCmax = 256 * P2;
+      G.T = std::min<int64_t>(G.NCmax - w + 1, N);
+      if (const char* tt = getenv("PASTILA_TILE_T")) { int64_t v = atoll(tt); if (v >= 1 && v < G.T) G.T = v; }
+      G.ntile = (N + G.T - 1) / G.T;
+      G.R = ((G.T + 31) / 32) | 1;
+      G.Tp = 32 * G.R;
+      G.smem_d = smem_rowsP(l, w, 256, P2, 8);
+      return PST_OK;
+    }
+  }
   // tile geometry: NC = NT*P columns, T = NC - w + 1 windows; aim for T >= 4w
   int nt = (4 * w > 256 * 5) ? 512 : 256;
   if (w > 160 && w <= 288) {
@@ -1600,7 +1948,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     a.dbg_ba = c->dbg;
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
   }
-  const size_t smem = smem_row1(chm == 0, l, w, NCmax, SV);
+  const size_t smem = G.v2 ? smem_rowsP(l, w, 256, P, SV) : smem_row1(chm == 0, l, w, NCmax, SV);
   const size_t smem2 = smem_row2(l, w, NCmax, SV);
   // the selection stream starts after everything queued before on the main stream
   PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
@@ -1618,7 +1966,9 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     dim3 grid((unsigned)ntile, (unsigned)ns);
     PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[bi], 0));  // buffer bi free again
     int r;
-    if (G.rows2)
+    if (G.v2)
+      r = (P == 8) ? launch_rowsP<8, V>(c, a, grid, smem) : launch_rowsP<4, V>(c, a, grid, smem);
+    else if (G.rows2)
       r = (nt == 512) ? launch_nt2<512, V>(c, a, grid, chm, smem2) : launch_nt2<256, V>(c, a, grid, chm, smem2);
     else
       r = (nt == 512) ? launch_nt<512, V>(c, a, grid, P, chm, smem)
@@ -1649,6 +1999,7 @@ int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64
   a.df = c->L.df; a.dg = c->L.dg;
   a.l = l; a.m = m; a.w = w; a.k = k; a.N = G.N; a.T = G.T;
   a.seg = seg_dev; a.win = win_dev; a.out = out_dev;
+  a.sumfixed = G.v2 ? 1 : 0;
   const size_t smem = (size_t)(l + 2 * (2 * w - 1) + 3 * w + 2 * (WX_NT / 32) + 2) * sizeof(double);
   const size_t smax = c->smem_optin ? c->smem_optin : 232448;
   if (smem > smax) {

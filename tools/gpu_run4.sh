@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_keys.py tests/test_gpu_parity.py -x -q 2>&1 | tail -5
+MODES=keys python tools/len_times.py 64 256 512 2>&1 | tail -3
+MODES=keys PASTILA_SEL=0 python tools/len_times.py 64 256 512 2>&1 | tail -3

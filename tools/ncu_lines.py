@@ -47,8 +47,16 @@ for cb in cubins:
             addr2line[(cur, int(m.group(1), 16))] = line
 funcs = sorted({f for f, _ in addr2line})
 # match the template arguments of the profiled kernel, e.g. "<(int)5, (int)256, (int)5>"
-targs = re.findall(r"\(int\)(-?\d+)", kname)
-want = "".join(f"Li{v}E" for v in targs)
+# mangled name of the profiled instantiation, e.g. "8k_mpdistILi5ELi256ELi5EiE"
+mb = re.search(r"::(\w+)<(.*)>\(", kname) or re.search(r"(\w+)<(.*)>\(", kname)
+want = None
+if mb:
+    enc = []
+    for t in [a.strip() for a in mb.group(2).split(",")]:
+        mi = re.match(r"\(int\)(-?\d+)", t)
+        mb2 = re.match(r"\(bool\)(\d)", t)
+        enc.append(f"Li{mi.group(1)}E" if mi else f"Lb{mb2.group(1)}E" if mb2 else {"int": "i", "double": "d"}.get(t, ""))
+    want = f"{len(mb.group(1))}{mb.group(1)}I{''.join(enc)}E"
 cands = [f for f in funcs if want and want in f] or funcs
 best = None
 for f in cands:

@@ -128,10 +128,29 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def host_cpu():
+    """Host core count and CPU model of this box (lscpu), stated next to every CPU number."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count() or 1
+    return {"os_cpu_count": os.cpu_count(), "usable_cores": usable, "model": model}
+
+
 def fp64_peak():
-    p = ROOT / "profiles" / "r01_fp64_peak.json"
-    if p.exists():
-        return float(json.loads(p.read_text())["fp64_fma_tflops"]), "measured (profiles/r01_fp64_peak.json, tools/fpeak.cu)"
+    for name in ("r02_fp64_peak.json", "r01_fp64_peak.json"):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            return float(json.loads(p.read_text())["fp64_fma_tflops"]), f"measured (profiles/{name}, tools/fpeak.cu)"
     return 37.0, "datasheet"
 
 
@@ -167,13 +186,16 @@ def run_reference(args):
     from concurrent.futures import ProcessPoolExecutor
 
     x = workload()
-    cores = os.cpu_count() or 1
-    jobs = [(m, i) for i, m in enumerate(GRID)][: max(1, cores)]
-    # each job: one segment of one length, windows restricted to a 100k-sample slice
+    host = host_cpu()
+    cores = max(1, host["usable_cores"])
+    # one job per usable core: (length, segment) pairs cycling through the C3 grid,
+    # each the MPdist profile of one segment over a 100k-sample slice of the C3 series
+    jobs = [(GRID[i % len(GRID)], 3 + i // len(GRID)) for i in range(cores)]
+
     def step():
         t0 = time.perf_counter()
-        with ProcessPoolExecutor(max_workers=min(cores, len(jobs))) as pool:
-            tot = sum(pool.map(_ref_job, [(m, i) for m, i in jobs]))
+        with ProcessPoolExecutor(max_workers=cores) as pool:
+            tot = sum(pool.map(_ref_job, jobs))
         return tot, time.perf_counter() - t0
     for _ in range(args.warmup):
         step()
@@ -188,9 +210,10 @@ def run_reference(args):
             "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(ws),
-            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": min(cores, len(jobs)), "kind": "port",
-                             "sample": f"{len(jobs)} jobs (one per length of the C3 grid, one per core): "
-                                       "MPdist profile of segment 3 over the first 100000 samples of the C3 series"},
+            "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": cores, "kind": "port", "host": host,
+                             "sample": f"{len(jobs)} jobs, one per usable core: (length, segment) pairs cycling "
+                                       "through the 15 C3 lengths, each the MPdist profile of one segment over "
+                                       "the first 100000 samples of the C3 series"},
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -200,11 +223,11 @@ def _ref_job(arg):
     os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import pastila_oracle as O
 
-    m, _ = arg
+    m, seg = arg
     x = workload()[:100_000]
     l, k = O.window_default(m), O.order_default(m)
     st = O.sliding_stats(x, l)
-    O.mpdist_profile(x, 3, m, l, k, st, col_chunk=25_000)
+    O.mpdist_profile(x, seg % (x.size // m), m, l, k, st, col_chunk=25_000)
     return (m - l + 1) * (x.size - l + 1)
 
 
@@ -277,6 +300,8 @@ def main():
     ctx.call("pst_sync")
     barrier()
     ctx.call("pst_timing", 1)
+    cert0 = np.zeros(8, dtype=np.int64)
+    ctx.call("pst_cert_stats", _native.ptr(cert0, C.c_int64), 1)  # reset the certification counters
     l0 = ctx.launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -294,6 +319,8 @@ def main():
     ctx.call("pst_timing_read", C.byref(kms), C.byref(klaunch))
     ctx.call("pst_timing", 0)
     launches = ctx.launches() - l0
+    cert = np.zeros(8, dtype=np.int64)
+    ctx.call("pst_cert_stats", _native.ptr(cert, C.c_int64), 0)
     barrier()
     if ws > 1 or args.force_dist:
         t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
@@ -338,10 +365,11 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         v, sample = cpu_sample_pairs_per_s(x)
-        cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample}
+        cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample, "host": host_cpu()}
     issue = None
-    ip = ROOT / "profiles" / "r01_full_g256_summary.json"
-    if ip.exists() and achieved:
+    ip = next((ROOT / "profiles" / f for f in ("r02_full_m256_summary.json", "r01_full_g256_summary.json")
+               if (ROOT / "profiles" / f).exists()), None)
+    if ip is not None and achieved:
         # secondary roofline: the path is bound by instruction issue (order
         # comparisons, van Herk minima, selection counts), not by FP64 flops
         wipp = sum(l["warp_instructions_per_pair"] for l in json.loads(ip.read_text())["launches"])
@@ -350,26 +378,32 @@ def main():
         peak_issue = 148 * 4 * sm_mhz * 1e6  # warp instructions / s (1 per scheduler per clock)
         issue = {"warp_instr_per_pair": wipp, "achieved": pps * wipp, "peak": peak_issue,
                  "unit": "warp-instr/s", "frac": pps * wipp / peak_issue,
-                 "source": "instructions per pair from profiles/r01_full_g256_summary.json (ncu, m=256 batch)"}
+                 "source": f"instructions per pair from profiles/{ip.name} (ncu, m=256 batch: row loop + selection)"}
     if rank == 0:
         traffic = None
-        tp = ROOT / "profiles" / "r01_traffic.json"
-        if tp.exists():
+        tp = next((ROOT / "profiles" / f for f in ("r02_traffic.json", "r01_traffic.json")
+                   if (ROOT / "profiles" / f).exists()), None)
+        if tp is not None:
             traffic = json.loads(tp.read_text()).get("bytes_per_launch")
         line = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "seconds_per_sweep": ms / 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config(ws, args.shard),
+            "config": _config(ws, args.shard), "host": host_cpu(),
             "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "seconds": e2e_s,
                     "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)},
-            "roofline": {"bound": "fp64", "kernel": "k_mpdist (profile tile kernel)",
+            "roofline": {"bound": "fp64", "kernel": "profile pass (k_mpdist<int> row loop + k_select_run<int> "
+                                                    "selection, key path)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "flops_per_pair": FP64_FLOPS_PER_PAIR, "peak_source": peak_src,
                          "kernel_ms_per_step": kms.value / args.steps,
                          "kernel_share_of_step": (kms.value / args.steps) / ms, "issue": issue},
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": int(launches),
+            "certification": {"per_step": {k: int(v) // max(1, args.steps) for k, v in zip(
+                ["lengths", "greedy_exact_candidates", "greedy_steps_multi", "attribution_uncertain_windows",
+                 "exact_window_evals", "max_candidates", "fallbacks_to_exact", "windows"], cert.tolist())},
+                "meaning": "key-path decisions resolved with exact fp64 values (pastila.cu run_select_keys)"},
             "m_best": max(e2e_res.items(), key=lambda t: (t[1], -t[0]))[0],
         }
         if args.grid:

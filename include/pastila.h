@@ -150,6 +150,9 @@ int pst_window_exact(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, const int64_
  * candidate, uncertain attribution windows, exact window evaluations,
  * profile_max candidates, fallbacks to the exact path, windows].         */
 int pst_cert_stats(pst_ctx* ctx, int64_t* out8, int reset);
+/* Instrumentation: milliseconds of the profile row-loop and selection
+ * kernels since the last call (needs PASTILA_KTIME=1 and pst_timing on).  */
+int pst_kernel_times(pst_ctx* ctx, double* out2);
 /* The context's CUDA stream (cudaStream_t) for caller-side event timing.  */
 int pst_stream(pst_ctx* ctx, void** stream_out);
 /* Profile-kernel timing: pst_timing(ctx,1) enables + resets; pst_timing_read

@@ -59,6 +59,8 @@ SIGNATURES = {
     "pst_profile_keys": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _ip]),
     "pst_window_exact": (C.c_int, [_vp, _i64, _i64, _i64, _lp, _lp, _i64, _dp]),
     "pst_cert_stats": (C.c_int, [_vp, _lp, C.c_int]),
+    "pst_kernel_times": (C.c_int, [_vp, _dp]),
+    "pst_debug_hist": (C.c_int, [_vp, _lp]),
     "pst_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "pst_timing": (C.c_int, [_vp, C.c_int]),
     "pst_timing_read": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),

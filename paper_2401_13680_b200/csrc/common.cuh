@@ -48,6 +48,7 @@ struct LenData {
   double* df = nullptr;     // (x[i+l]-x[i])/2
   double* dg = nullptr;     // (x[i+l]-mc[i+1]) + (x[i]-mc[i])
   double* mc = nullptr;     // direct window mean sum(x)/l (centering of the distance kernels)
+  unsigned long long* hash = nullptr;  // 64-bit polynomial hash of the window's bit patterns (exact repeats)
 };
 
 struct pst_ctx {
@@ -89,6 +90,9 @@ struct pst_ctx {
   void* tev = nullptr;  // std::vector<std::pair<cudaEvent_t,cudaEvent_t>>*
   double t_ms = 0.0;
   int64_t t_calls = 0, t_launch = 0;
+  // per-kernel-class event timing (PASTILA_KTIME=1, instrumentation): row loop vs selection
+  void* kev = nullptr;  // std::vector<KEv>*
+  double k_ms[2] = {0.0, 0.0};
   int num_sms = 148;
   size_t smem_optin = 0;
 };
@@ -101,6 +105,7 @@ int pst_ensure_len(pst_ctx* c, int64_t l);
 // (exact e values) or int (32-bit key = high word of e, see mpdist.cu).
 struct MPArgs {
   const double *x, *mu /* centering means (LenData::mc) */, *nrm, *bias, *cbias, *df, *dg;
+  const unsigned long long* hash;  // window hashes (exact-repeat zeros, see repeat_zero in mpdist.cu)
   int64_t n, l, m, w, k, Nl, N, T;
   int64_t seg0;      // segment of blockIdx.y == 0
   void* D;           // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y): double d / int key
@@ -134,5 +139,6 @@ int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_
                        int* Dk_dev, int64_t ld);
 // exact profile values at single (segment, window) pairs, bit-identical to the
 // full profile kernels: out[i] = D[seg[i]][win[i]] (device arrays, cnt entries).
+int kernel_times_read(pst_ctx* c, double* out2);
 int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* seg_dev,
                         const int64_t* win_dev, int64_t cnt, double* out_dev);

@@ -80,6 +80,34 @@ struct VT<int> {
   static __device__ __forceinline__ int quarter(int v) { return v - (2 << 20); }  // e/4: exponent - 2
 };
 
+// Exact repeats: bit-equal windows at different positions are at distance 0
+// wherever they sit (zdist.py:98-106).  The correlation path leaves a rounding
+// residue there (up to ~1e-13 for long windows), so every e below 1e-10 is
+// checked against the window hashes and, on a match, the samples themselves.
+// Tiny e is rare, so the check is one integer compare per pair on the fast path.
+constexpr int KEY_E10 = 0x3DDB7CDF;  // high word of 1e-10
+__device__ __noinline__ double repeat_zero(double e, const double* __restrict__ x,
+                                           const unsigned long long* __restrict__ hash, int64_t q, int64_t c, int l) {
+  if (q == c || hash[q] != hash[c]) return e;
+  for (int t = 0; t < l; ++t)
+    if (__double_as_longlong(x[q + t]) != __double_as_longlong(x[c + t])) return e;
+  return 0.0;
+}
+__device__ __forceinline__ double fixrep(double e, const MPArgs& a, int64_t q, int64_t c) {
+  return (__double2hiint(e) < KEY_E10) ? repeat_zero(e, a.x, a.hash, q, c, (int)a.l) : e;
+}
+// one row's P values of a thread: a single branch on the smallest high word
+template <int P>
+__device__ __forceinline__ void fixrep_row(double (&ed)[P], const MPArgs& a, int64_t q, int64_t c0) {
+  int mh = __double2hiint(ed[0]);
+#pragma unroll
+  for (int p = 1; p < P; ++p) mh = min(mh, __double2hiint(ed[p]));
+  if (mh < KEY_E10) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) ed[p] = fixrep(ed[p], a, q, c0 + p);
+  }
+}
+
 // ---------------------------------------------------------------- selection
 // Exact k-th smallest (1-based) of the 2w-element P_ABBA multiset of one
 // window (mpdist.py:224-231): A = w row minima (AB scratch), B = w column
@@ -645,9 +673,13 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     V* Et = E + tid * P;
     if (nq != 0.0) {
       const double mnq = -nq;
+      double ed[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) ed[p] = fma(cov[p] * mnq, nrmc[p], bic[p]);
+      fixrep_row<P>(ed, a, q0 + i, J0 + tid * P);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const V e = VT<V>::of(fma(cov[p] * mnq, nrmc[p], bic[p]));
+        const V e = VT<V>::of(ed[p]);
         colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
@@ -711,7 +743,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   {
     V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
     for (int c = tid; c < NC; c += NT) bag[c] = E[c];
-    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+    if (a.dbg_ba && !(a.dbg_flags & 16) && blockIdx.x == 0 && blockIdx.y == 0)
       for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = E[c];
   }
 }
@@ -851,9 +883,13 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     const double nq = rnq[i];
     if (nq != 0.0) {
       const double mnq = -nq;
+      double ed[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) ed[p] = fma(cv[p] * mnq, nrmc[p], bic[p]);
+      fixrep_row<P>(ed, a, q0 + i, J0 + tid * P);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const V e = VT<V>::of(fma(cv[p] * mnq, nrmc[p], bic[p]));
+        const V e = VT<V>::of(ed[p]);
         colmin[p] = vmin(colmin[p], e);
         Et[p] = e;
       }
@@ -938,7 +974,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   {
     V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
     for (int c = tid; c < NC; c += NT) bag[c] = E[c];
-    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+    if (a.dbg_ba && !(a.dbg_flags & 16) && blockIdx.x == 0 && blockIdx.y == 0)
       for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = E[c];
   }
 }
@@ -1100,14 +1136,17 @@ __global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPAr
     V kk[P];
     if (nq != 0.0) {
       const double mnq = -nq;
+      double ed[P];
       if (!cst_tile) {  // every column non-constant: bias 1.0
 #pragma unroll
-        for (int p = 0; p < P; ++p) kk[p] = VT<V>::of(fma(cov[p] * mnq, nrmc[p], 1.0));
+        for (int p = 0; p < P; ++p) ed[p] = fma(cov[p] * mnq, nrmc[p], 1.0);
       } else {
 #pragma unroll
-        for (int p = 0; p < P; ++p)
-          kk[p] = VT<V>::of(fma(cov[p] * mnq, nrmc[p], (c0 + p < NC) ? a.bias[J0 + c0 + p] : PST_INF));
+        for (int p = 0; p < P; ++p) ed[p] = fma(cov[p] * mnq, nrmc[p], (c0 + p < NC) ? a.bias[J0 + c0 + p] : PST_INF);
       }
+      fixrep_row<P>(ed, a, q0 + i, J0 + c0);
+#pragma unroll
+      for (int p = 0; p < P; ++p) kk[p] = VT<V>::of(ed[p]);
     } else {  // constant query window (row-uniform branch): zdist.py:111-112
 #pragma unroll
       for (int p = 0; p < P; ++p) kk[p] = (c0 + p < NC) ? VT<V>::of(a.cbias[J0 + c0 + p]) : VT<V>::inf();
@@ -1171,7 +1210,7 @@ __global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPAr
   {
     V* bag = (V*)a.ba + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * NCmax;
     for (int c = tid; c < NC; c += NT) bag[c] = BAs[c];
-    if (a.dbg_ba && blockIdx.x == 0 && blockIdx.y == 0)
+    if (a.dbg_ba && !(a.dbg_flags & 16) && blockIdx.x == 0 && blockIdx.y == 0)
       for (int c = tid; c < NC; c += NT) ((V*)a.dbg_ba)[c] = BAs[c];
   }
 }
@@ -1428,6 +1467,11 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
       }
       V ans = p;
       bool done = lt < k && k <= le;
+      if (a.dbg_ba && (a.dbg_flags & 16) && ok) {  // instrumentation: rank-move histogram (PASTILA_DBGF=16)
+        const int mv = (lt < k && k <= le) ? 0 : (k <= lt ? lt - k + 1 : k - le);
+        const int b = mv == 0 ? 0 : mv == 1 ? 1 : mv == 2 ? 2 : mv <= 4 ? 3 : mv <= 8 ? 4 : mv <= 16 ? 5 : 6;
+        atomicAdd((unsigned long long*)a.dbg_ba + b, 1ull);
+      }
       if (!done) {
         if (k <= lt) {
           const int need = lt - k + 1;  // rank from the top among the values below p
@@ -1504,6 +1548,7 @@ __global__ void __launch_bounds__(NWS * 32, 1) k_select_run(const MPArgs a, int 
 // Used to resolve the decisions the key path cannot certify (pastila.cu).
 struct WinArgs {
   const double *x, *mu, *nrm, *bias, *cbias, *df, *dg;
+  const unsigned long long* hash;
   int64_t l, m, w, k, N, T;
   int sumfixed;  // 1: centered-window sums by warp_sum_fixed (k_rowsP tiles), 0: sequential (k_mpdist)
   const int64_t *seg, *win;
@@ -1603,6 +1648,7 @@ __global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
       if (i > 0) cur[u] = cvv;
       if (cl >= jl) {
         double e = (nq != 0.0) ? fma(cvv * (-nq), a.nrm[c], a.bias[c]) : a.cbias[c];
+        if (nq != 0.0 && __double2hiint(e) < KEY_E10) e = repeat_zero(e, a.x, a.hash, q, c, l);
         if (c == q) e = 0.0;
         rm = vmin(rm, e);
         BAc[cl - jl] = vmin(BAc[cl - jl], e);  // column owned by this thread
@@ -1902,10 +1948,35 @@ int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_
   return launch_timed<int>(c, m, l, k, seg_lo, seg_hi, Dk_dev, ld);
 }
 
+struct KEv {
+  cudaEvent_t e0, e1;
+  int kind;  // 0 = row loop, 1 = selection
+};
+// events around one launch on stream st (PASTILA_KTIME=1 with pst_timing enabled)
+static bool ktime_on(pst_ctx* c) {
+  static const bool env = getenv("PASTILA_KTIME") && atoi(getenv("PASTILA_KTIME")) > 0;
+  return env && c->timing;
+}
+static int kev_begin(pst_ctx* c, cudaStream_t st, KEv& e, int kind) {
+  e.kind = kind;
+  PST_CUDA(cudaEventCreate(&e.e0));
+  PST_CUDA(cudaEventCreate(&e.e1));
+  PST_CUDA(cudaEventRecord(e.e0, st));
+  return PST_OK;
+}
+static int kev_end(pst_ctx* c, cudaStream_t st, KEv& e) {
+  PST_CUDA(cudaEventRecord(e.e1, st));
+  if (!c->kev) c->kev = new std::vector<KEv>();
+  ((std::vector<KEv>*)c->kev)->push_back(e);
+  return PST_OK;
+}
+
 template <class V>
 static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
                               void* D_dev, int64_t ld) {
   const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
+  const bool kt = ktime_on(c);
+  KEv ke;
   TileGeom G;
   PST_TRY(tile_geom(c, m, l, G));
   const int nt = G.nt, P = G.P, chm = G.chm;
@@ -1937,13 +2008,16 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   }
   MPArgs a;
   a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
-  a.df = c->L.df; a.dg = c->L.dg;
+  a.df = c->L.df; a.dg = c->L.dg; a.hash = c->L.hash;
   a.n = n; a.l = l; a.m = m; a.w = w; a.k = k; a.Nl = Nl; a.N = N; a.T = T;
   a.R = R; a.Tp = Tp;
   a.D = D_dev; a.ldD = ld;
   a.dbg_ba = nullptr;
   a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
-  if (getenv("PASTILA_DEBUG")) {
+  if (a.dbg_flags & 16) {  // move histogram: 8 counters, read with pst_debug_hist
+    PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8 > 64 ? (size_t)NCmax * 8 : 64));
+    a.dbg_ba = c->dbg;
+  } else if (getenv("PASTILA_DEBUG")) {
     PST_TRY(pst_ensure((void**)&c->dbg, &c->dbg_bytes, (size_t)NCmax * 8));
     a.dbg_ba = c->dbg;
     c->dbg_T = T; c->dbg_NC = std::min(T, N) + w - 1; c->dbg_w = w;
@@ -1965,6 +2039,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     a.ba = buf + ab_cta * (size_t)ntile * (size_t)segs_per;
     dim3 grid((unsigned)ntile, (unsigned)ns);
     PST_CUDA(cudaStreamWaitEvent(c->st, c->ev_sel[bi], 0));  // buffer bi free again
+    if (kt) PST_TRY(kev_begin(c, c->st, ke, 0));
     int r;
     if (G.v2)
       r = (P == 8) ? launch_rowsP<8, V>(c, a, grid, smem) : launch_rowsP<4, V>(c, a, grid, smem);
@@ -1975,10 +2050,13 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
           : (nt == 128) ? launch_nt<128, V>(c, a, grid, P, chm, smem)
                         : launch_nt<256, V>(c, a, grid, P, chm, smem);
     if (r != PST_OK) return r;
+    if (kt) PST_TRY(kev_end(c, c->st, ke));
     PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
     PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));
+    if (kt) PST_TRY(kev_begin(c, c->st2, ke, 1));
     r = launch_sel<V>(c, a, grid, (int)NCmax);
     if (r != PST_OK) return r;
+    if (kt) PST_TRY(kev_end(c, c->st2, ke));
     PST_CUDA(cudaEventRecord(c->ev_sel[bi], c->st2));
   }
   // the main stream continues only after all selections
@@ -1996,7 +2074,7 @@ int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64
   const int64_t w = G.w;
   WinArgs a;
   a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
-  a.df = c->L.df; a.dg = c->L.dg;
+  a.df = c->L.df; a.dg = c->L.dg; a.hash = c->L.hash;
   a.l = l; a.m = m; a.w = w; a.k = k; a.N = G.N; a.T = G.T;
   a.seg = seg_dev; a.win = win_dev; a.out = out_dev;
   a.sumfixed = G.v2 ? 1 : 0;
@@ -2016,5 +2094,25 @@ int launch_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64
     c->launches++;
     PST_CUDA(cudaGetLastError());
   }
+  return PST_OK;
+}
+
+// accumulated row-loop / selection kernel milliseconds (PASTILA_KTIME=1), reset after reading
+int kernel_times_read(pst_ctx* c, double* out2) {
+  PST_CUDA(cudaDeviceSynchronize());
+  if (c->kev) {
+    auto* v = (std::vector<KEv>*)c->kev;
+    for (auto& e : *v) {
+      float f = 0.f;
+      PST_CUDA(cudaEventElapsedTime(&f, e.e0, e.e1));
+      c->k_ms[e.kind] += f;
+      cudaEventDestroy(e.e0);
+      cudaEventDestroy(e.e1);
+    }
+    v->clear();
+  }
+  out2[0] = c->k_ms[0];
+  out2[1] = c->k_ms[1];
+  c->k_ms[0] = c->k_ms[1] = 0.0;
   return PST_OK;
 }

@@ -141,6 +141,17 @@ __global__ void k_dfdg(const double* __restrict__ x, int64_t n, int64_t l, LenDa
   }
 }
 
+// Window hashes for the exact-repeat rule (zdist.py:98-106: bit-equal windows are
+// at distance 0 wherever they sit): Horner over the l sample bit patterns, mod 2^64.
+__global__ void k_hash(const double* __restrict__ x, int64_t n, int64_t l, unsigned long long* hash) {
+  const int64_t Nl = n - l + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Nl; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long h = 0;
+    for (int64_t t = 0; t < l; ++t) h = h * 0x9E3779B97F4A7C15ull + (unsigned long long)__double_as_longlong(x[i + t]);
+    hash[i] = h;
+  }
+}
+
 // Distance rows for queries q0..q0+rows-1 (zdist.py:191-225): one thread per
 // diagonal; diagonals entering at row 0 (column c0 >= 0) or at column 0
 // (row r0 > 0) start from a fresh centered dot product.
@@ -172,6 +183,11 @@ __global__ void k_rows(const double* __restrict__ x, LenData L, int64_t n, int64
       e = L.cbias[c];
     else
       e = fma(-(cov * nq), L.nrm[c], L.bias[c]);
+    if (e < 1e-10 && c != q && L.hash[q] == L.hash[c]) {  // exact repeat (bit-equal windows): d = 0
+      bool same = true;
+      for (int64_t t = 0; t < l && same; ++t) same = __double_as_longlong(x[q + t]) == __double_as_longlong(x[c + t]);
+      if (same) e = 0.0;
+    }
     if (c == q) e = 0.0;
     e = clamp0(e);
     if (e < 1e-15) e = 0.0;
@@ -661,7 +677,8 @@ int pst_ensure_len(pst_ctx* c, int64_t l) {
   if (c->L.l == l) return PST_OK;
   const int64_t Nl = c->n - l + 1;
   if (Nl > c->cap_l) {
-    double** arrs[] = {&c->L.mu, &c->L.var, &c->L.sd, &c->L.nrm, &c->L.bias, &c->L.cbias, &c->L.df, &c->L.dg, &c->L.mc};
+    double** arrs[] = {&c->L.mu, &c->L.var, &c->L.sd, &c->L.nrm, &c->L.bias, &c->L.cbias, &c->L.df, &c->L.dg, &c->L.mc,
+                       (double**)&c->L.hash};
     for (double** a : arrs) {
       if (*a) cudaFree(*a);
       *a = nullptr;
@@ -678,7 +695,8 @@ int pst_ensure_len(pst_ctx* c, int64_t l) {
   }
   k_stats<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->csum, c->csq, c->chg, c->n, l, c->L);
   k_dfdg<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->n, l, c->L);
-  c->launches += 2;
+  k_hash<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->n, l, c->L.hash);
+  c->launches += 3;
   PST_CUDA(cudaGetLastError());
   c->L.l = l;
   c->L.Nl = Nl;
@@ -1619,6 +1637,13 @@ int pst_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t*
   return PST_OK;
 }
 
+// Row-loop / selection kernel milliseconds since the last read (PASTILA_KTIME=1 and
+// pst_timing enabled; instrumentation only: events around every launch).
+int pst_kernel_times(pst_ctx* c, double* out2) {
+  if (!valid(c)) return PST_EINVAL;
+  return kernel_times_read(c, out2);
+}
+
 // The context's CUDA stream (cudaStream_t), for event timing by callers.
 int pst_stream(pst_ctx* c, void** out) {
   if (!valid(c)) return PST_EINVAL;
@@ -1662,6 +1687,15 @@ int pst_timing_read(pst_ctx* c, double* ms, int64_t* launches) {
   }
   *ms = c->t_ms;
   *launches = c->t_launch;
+  return PST_OK;
+}
+
+// debug: rank-move histogram of the selection (PASTILA_DBGF=16): 8 counters, read and cleared
+int pst_debug_hist(pst_ctx* c, int64_t* out8) {
+  if (!c->dbg) { pst_set_error("PASTILA_DBGF=16 not set"); return PST_ESTATE; }
+  PST_CUDA(cudaDeviceSynchronize());
+  PST_CUDA(cudaMemcpy(out8, c->dbg, 64, cudaMemcpyDeviceToHost));
+  PST_CUDA(cudaMemset(c->dbg, 0, 64));
   return PST_OK;
 }
 

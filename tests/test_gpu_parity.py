@@ -192,6 +192,14 @@ def test_select_length_c2_planted_walk(golden_c2):
         assert [s.index for s in r.snippets] == doc["indices"]
         assert [s.frac for s in r.snippets] == doc["fracs"]
         assert r.unassigned_windows == doc["unassigned_windows"]
+    # labels of the winning length (labeling.py:91-119) from the oracle's profiles of the chosen segments
+    w = results[rep.m_best]
+    pr = P.MPdistParams(rep.m_best)
+    st = O.sliding_stats(x, pr.window_size)
+    prof = [O.mpdist_profile(x, s.index, rep.m_best, pr.window_size, pr.k, st) for s in w.snippets]
+    for a, b in zip(w.profiles, prof):
+        np.testing.assert_allclose(a.values, b, atol=1e-6)
+    assert np.array_equal(P.label_series(w).labels, O.labels(prof, x.size))
 
 
 def test_exact_ties_two_regime():

@@ -1,0 +1,165 @@
+"""Parity at the headline scales: sampled-segment MPdist
+profiles at the true n against the CPU oracle (oracle/pastila_oracle.py, the
+numpy restatement of mpdist.py:179-232 pinned to the reference's golden
+vectors), for the C3 workload (n = 1e6, planted walk m_act = 256, A = 4) and
+a C5 long-window length (n = 2e6); the key path's buckets and the exact
+single-window evaluator are checked at the same segments.  C4 (n = 1e7) runs
+with PASTILA_SCALE_C4=1 (minutes of oracle time; its result is recorded in
+profiles/r02_scale_parity.json by tools/scale_parity.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import paper_2401_13680_b200 as P
+from oracle import pastila_oracle as O
+from paper_2401_13680_b200 import _native
+from paper_2401_13680_b200.datagen import planted_walk
+
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-6   # north_star: MPdist values within 1e-6 (fp64)
+RTOL = 1e-6
+
+
+def _gpu_profile(x, m, seg):
+    pr = P.MPdistParams(m)
+    out = np.empty((1, x.size - m + 1))
+    with _native.context().using(x) as ctx:
+        ctx.call("pst_mpdist_profiles", m, pr.window_size, pr.k, seg, seg + 1, _native.ptr(out))
+    return out[0]
+
+
+def _gpu_keys(x, m, seg):
+    pr = P.MPdistParams(m)
+    out = np.empty((1, x.size - m + 1), dtype=np.int32)
+    with _native.context().using(x) as ctx:
+        ctx.call("pst_profile_keys", m, pr.window_size, pr.k, seg, seg + 1, _native.ptr(out, C.c_int32))
+    return out[0]
+
+
+def _window_exact(x, m, seg, win):
+    pr = P.MPdistParams(m)
+    s = np.full(win.size, seg, dtype=np.int64)
+    wv = np.ascontiguousarray(win, dtype=np.int64)
+    out = np.empty(win.size)
+    with _native.context().using(x) as ctx:
+        ctx.call("pst_window_exact", m, pr.window_size, pr.k, _native.ptr(s, C.c_int64),
+                 _native.ptr(wv, C.c_int64), s.size, _native.ptr(out))
+    return out
+
+
+def _bucket(keys, l):
+    k64 = keys.astype(np.int64)
+    lo_bits = (k64 & 0xFFFFFFFF) << 32
+
+    def f(e):
+        e = np.where(e < 1e-15, 0.0, e)
+        e = np.where(e > 2.0, 2.0, e)
+        return np.sqrt((2.0 * l) * e)
+
+    lo = f(lo_bits.astype(np.uint64).view(np.float64))
+    hi = f((lo_bits | 0xFFFFFFFF).astype(np.uint64).view(np.float64))
+    return np.where(keys < 0, 0.0, lo), np.where(keys < 0, 0.0, hi)
+
+
+def _check_segment(x, m, seg, stats, col_chunk):
+    pr = P.MPdistParams(m)
+    ref = O.mpdist_profile(x, seg, m, pr.window_size, pr.k, stats, col_chunk=col_chunk)
+    got = _gpu_profile(x, m, seg)
+    np.testing.assert_allclose(got, ref, atol=ATOL, rtol=RTOL)
+    keys = _gpu_keys(x, m, seg)
+    lo, hi = _bucket(keys, pr.window_size)
+    assert np.all(lo <= got) and np.all(got <= hi)
+    rng = np.random.default_rng(seg * 7919 + m)
+    win = np.unique(np.concatenate([rng.integers(0, got.size, 48), [0, got.size - 1]]))
+    assert np.array_equal(_window_exact(x, m, seg, win), got[win])
+    return float(np.max(np.abs(got - ref)))
+
+
+@pytest.fixture(scope="module")
+def c3_series():
+    x, _ = planted_walk(1_000_000, m_act=256, A=4, seed=0)
+    return x
+
+
+@pytest.mark.parametrize("m", [64, 256, 512])
+def test_c3_sampled_segments_vs_oracle(c3_series, m):
+    x = c3_series
+    S = x.size // m
+    segs = [1, S // 2, S - 1] if m < 512 else [1, S - 1]
+    st = O.sliding_stats(x, P.MPdistParams(m).window_size)
+    for s in segs:
+        _check_segment(x, m, s, st, col_chunk=100_000)
+
+
+def test_c5_long_window_segment_vs_oracle():
+    x, _ = planted_walk(2_000_000, m_act=2048, A=5, seed=0)
+    m = 1024
+    st = O.sliding_stats(x, P.MPdistParams(m).window_size)
+    _check_segment(x, m, (x.size // m) // 2, st, col_chunk=50_000)
+
+
+@pytest.mark.skipif(os.environ.get("PASTILA_SCALE_C4") != "1", reason="C4 oracle segment takes minutes")
+def test_c4_segment_vs_oracle():
+    x, _ = planted_walk(10_000_000, m_act=256, A=3, seed=0)  # tools/c4_run.py
+    m = 256
+    st = O.sliding_stats(x, P.MPdistParams(m).window_size)
+    _check_segment(x, m, (x.size // m) // 2, st, col_chunk=200_000)
+
+
+def _direct_mpdist(x, m, seg, windows):
+    """MPdist values at the given windows from DIRECT z-normalized distance rows
+    (explicit per-window mean/std, pst_distance_rows method 1): no correlation
+    identity, so no cancellation near d = 0 -- the exact value to judge against."""
+    pr = P.MPdistParams(m)
+    l, k = pr.window_size, pr.k
+    w, q0, Nl = m - l + 1, seg * m, x.size - l + 1
+    rows = np.empty((w, Nl))
+    with _native.context().using(x) as ctx:
+        ctx.call("pst_distance_rows", l, q0, w, 1, _native.ptr(rows))
+    colmin = rows.min(axis=0)
+    cols = np.arange(Nl)
+    colmin[(cols >= q0) & (cols < q0 + w)] = 0.0
+    out = []
+    for j in windows:
+        ab = rows[:, j:j + w].min(axis=1)
+        v = np.concatenate([ab, colmin[j:j + w]])
+        out.append(np.partition(v, k - 1)[k - 1] if 2 * w > k else v.max())
+    return np.array(out)
+
+
+def test_long_window_exact_and_near_repeats():
+    """Long windows (l = 2048) with an exact and a near-exact (1e-12) repeat of a segment.
+
+    Near d = 0 the reference computes d = sqrt(2l(1 - rho)) from prefix-sum statistics
+    and its rounding of rho is amplified by the sqrt (here up to 8e-5 where the exact
+    distance is 1e-10).  The bar: within 1e-6 of the reference, or at least as close as
+    the reference to the exact value (direct z-normalized distances).  Identical content
+    must give bit-identical profiles (ties by lowest index).
+    """
+    m = 4096
+    rng = np.random.default_rng(11)
+    x = 0.05 * np.cumsum(rng.standard_normal(12 * m))
+    x[5 * m:6 * m] = x[1 * m:2 * m]                                         # exact repeat of segment 1
+    x[8 * m:9 * m] = x[1 * m:2 * m] + 1e-12 * rng.standard_normal(m)        # near repeat
+    pr = P.MPdistParams(m)
+    l = pr.window_size
+    st = O.sliding_stats(x, l)
+    for seg in (1, 5, 8):
+        ref = O.mpdist_profile(x, seg, m, l, pr.k, st, col_chunk=20_000)
+        got = _gpu_profile(x, m, seg)
+        far = np.flatnonzero(np.abs(got - ref) > ATOL)
+        if far.size:
+            pick = far[np.argsort(-np.abs(got - ref)[far])[:8]]
+            exact = _direct_mpdist(x, m, seg, pick)
+            assert np.all(np.abs(got[pick] - exact) <= np.abs(ref[pick] - exact) + 1e-9), (seg, pick)
+            assert np.all(ref[far] < 1e-3)  # deviations only in the near-zero region
+    p1, p5 = _gpu_profile(x, m, 1), _gpu_profile(x, m, 5)
+    assert p1[5 * m] <= 1e-6 and p5[1 * m] <= 1e-6  # the repeat is a zero-distance match
+    assert np.array_equal(p1, p5)  # identical content, identical profiles: exact ties stay ties

@@ -2,6 +2,7 @@
 // distance kernels; MEASURED_PEAKS.json only carries HBM and bf16).
 // Independent FMA chains per thread, grid = SMs * 8 CTAs, CUDA-event timed.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 template <typename T, int CH>
 __global__ void fma_loop(T* out, int iters, T a, T b) {
@@ -31,7 +32,8 @@ __global__ void mixed_loop(double* out, int iters, double a, double b) {
   for (int c = 0; c < 8; ++c) { s += acc[c]; t += u[c]; }
   if (s == 12345.678 || t == 7u) out[threadIdx.x] = s + t;
 }
-int main() {
+int main(int argc, char** argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 5;  // long runs: clocks sampled under load by tools/fpeak_run.py
   int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   int sms = p.multiProcessorCount;
   double* d; cudaMalloc(&d, 1 << 20);
@@ -39,7 +41,7 @@ int main() {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   int blocks = sms * 8, threads = 256, iters = 20000;
   double best64 = 0, best32 = 0, bestmix = 0;
-  for (int rep = 0; rep < 5; ++rep) {
+  for (int rep = 0; rep < reps; ++rep) {
     float ms;
     cudaEventRecord(e0); fma_loop<double, 8><<<blocks, threads>>>(d, iters, 0.999999, 1e-7); cudaEventRecord(e1);
     cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);

@@ -33,11 +33,13 @@ for m in ms:
         dt = time.perf_counter() - t0
         kms, kl = C.c_double(0), C.c_int64(0)
         ctx.call("pst_timing_read", C.byref(kms), C.byref(kl))
+        kt = np.zeros(2)
+        ctx.call("pst_kernel_times", _native.ptr(kt))
         ctx.call("pst_timing", 0)
         ctx.call("pst_cert_stats", _native.ptr(st, C.c_int64), 0)
         l = P.MPdistParams(m).window_size
         pairs = (m - l + 1) * (x.size - l + 1) * (x.size // m)
-        rec = {"m": m, "mode": mode, "total_s": dt, "profile_kernel_s": kms.value / 1e3,
+        rec = {"m": m, "mode": mode, "total_s": dt, "profile_kernel_s": kms.value / 1e3, "row_s": kt[0] / 1e3, "sel_s": kt[1] / 1e3,
                "pairs_per_s": pairs / dt, "snippets": [sn.index for sn in r.snippets],
                "cert": st.tolist()}
         out.append(rec)

@@ -49,6 +49,7 @@ struct LenData {
   double* dg = nullptr;     // (x[i+l]-mc[i+1]) + (x[i]-mc[i])
   double* mc = nullptr;     // direct window mean sum(x)/l (centering of the distance kernels)
   unsigned long long* hash = nullptr;  // 64-bit polynomial hash of the window's bit patterns (exact repeats)
+  bool has_rep = false;     // two windows share a hash (possible exact repeat): the rule must run
 };
 
 struct pst_ctx {
@@ -81,6 +82,8 @@ struct pst_ctx {
   int64_t cert_stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   void* work = nullptr;
   size_t work_bytes = 0;
+  void* aux = nullptr;       // per-length preparation scratch (hash sort); never holds live results
+  size_t aux_bytes = 0;
   int64_t launches = 0;
   double* dbg = nullptr;
   size_t dbg_bytes = 0;
@@ -105,7 +108,8 @@ int pst_ensure_len(pst_ctx* c, int64_t l);
 // (exact e values) or int (32-bit key = high word of e, see mpdist.cu).
 struct MPArgs {
   const double *x, *mu /* centering means (LenData::mc) */, *nrm, *bias, *cbias, *df, *dg;
-  const unsigned long long* hash;  // window hashes (exact-repeat zeros, see repeat_zero in mpdist.cu)
+  const unsigned long long* hash;  // window hashes (exact-repeat zeros, see same_window in mpdist.cu)
+  int rep;                         // apply the exact-repeat rule (always, except the A/B test knob)
   int64_t n, l, m, w, k, Nl, N, T;
   int64_t seg0;      // segment of blockIdx.y == 0
   void* D;           // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y): double d / int key

@@ -81,31 +81,43 @@ struct VT<int> {
 };
 
 // Exact repeats: bit-equal windows at different positions are at distance 0
-// wherever they sit (zdist.py:98-106).  The correlation path leaves a rounding
-// residue there (up to ~1e-13 for long windows), so every e below 1e-10 is
-// checked against the window hashes and, on a match, the samples themselves.
-// Tiny e is rare, so the check is one integer compare per pair on the fast path.
-constexpr int KEY_E10 = 0x3DDB7CDF;  // high word of 1e-10
-__device__ __noinline__ double repeat_zero(double e, const double* __restrict__ x,
-                                           const unsigned long long* __restrict__ hash, int64_t q, int64_t c, int l) {
-  if (q == c || hash[q] != hash[c]) return e;
+// wherever they sit (zdist.py:98-106); the correlation path would leave a
+// rounding residue there (up to ~1e-13 for long windows).  Each CTA marks,
+// once, the columns whose window hash may equal one of its w query-window
+// hashes (a 16384-bit, two-probe filter of the query hashes in shared
+// memory); only marked columns are checked per row (hash, then samples).
+constexpr int REP_WORDS = 512;
+__device__ __noinline__ bool same_window(const double* __restrict__ x, const unsigned long long* __restrict__ hash,
+                                         int64_t q, int64_t c, int l) {
+  if (q == c || hash[q] != hash[c]) return false;
   for (int t = 0; t < l; ++t)
-    if (__double_as_longlong(x[q + t]) != __double_as_longlong(x[c + t])) return e;
-  return 0.0;
+    if (__double_as_longlong(x[q + t]) != __double_as_longlong(x[c + t])) return false;
+  return true;
 }
-__device__ __forceinline__ double fixrep(double e, const MPArgs& a, int64_t q, int64_t c) {
-  return (__double2hiint(e) < KEY_E10) ? repeat_zero(e, a.x, a.hash, q, c, (int)a.l) : e;
+__device__ __forceinline__ bool rep_probe(const unsigned* rmap, unsigned long long h) {
+  const unsigned i1 = (unsigned)(h & 16383u), i2 = (unsigned)((h >> 20) & 16383u);
+  return ((rmap[i1 >> 5] >> (i1 & 31)) & (rmap[i2 >> 5] >> (i2 & 31)) & 1u) != 0u;
 }
-// one row's P values of a thread: a single branch on the smallest high word
-template <int P>
-__device__ __forceinline__ void fixrep_row(double (&ed)[P], const MPArgs& a, int64_t q, int64_t c0) {
-  int mh = __double2hiint(ed[0]);
-#pragma unroll
-  for (int p = 1; p < P; ++p) mh = min(mh, __double2hiint(ed[p]));
-  if (mh < KEY_E10) {
-#pragma unroll
-    for (int p = 0; p < P; ++p) ed[p] = fixrep(ed[p], a, q, c0 + p);
+// build the filter of the query hashes hash[q0 .. q0+w) (all threads; ends with a barrier)
+__device__ __forceinline__ void rep_build(unsigned* rmap, const unsigned long long* __restrict__ hash, int64_t q0,
+                                          int w, int tid, int nt) {
+  for (int b = tid; b < REP_WORDS; b += nt) rmap[b] = 0u;
+  __syncthreads();
+  for (int i = tid; i < w; i += nt) {
+    const unsigned long long h = hash[q0 + i];
+    const unsigned i1 = (unsigned)(h & 16383u), i2 = (unsigned)((h >> 20) & 16383u);
+    atomicOr(&rmap[i1 >> 5], 1u << (i1 & 31));
+    atomicOr(&rmap[i2 >> 5], 1u << (i2 & 31));
   }
+  __syncthreads();
+}
+// apply the rule to the marked columns of one row (rare path)
+template <int P>
+__device__ __noinline__ void rep_apply(double (&ed)[P], unsigned mask, const MPArgs& a, int64_t q, int64_t c0) {
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if ((mask >> p) & 1u)
+      if (same_window(a.x, a.hash, q, c0 + p, (int)a.l)) ed[p] = 0.0;
 }
 
 // ---------------------------------------------------------------- selection
@@ -632,7 +644,15 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     bic[p] = ok ? a.bias[c] : PST_INF;
     colmin[p] = VT<V>::inf();
   }
-  __syncthreads();
+  __shared__ unsigned rmap[REP_WORDS];
+  if (a.rep)
+    rep_build(rmap, a.hash, q0, w, tid, NT);  // ends with a barrier
+  else
+    __syncthreads();
+  unsigned repm = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (a.rep && tid * P + p < NC && rep_probe(rmap, a.hash[J0 + tid * P + p])) repm |= 1u << p;
 
   const int qloc = (int)(q0 - J0) - tid * P;  // my local index of the self column at row 0
   VHGeom g;
@@ -676,7 +696,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
       double ed[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) ed[p] = fma(cov[p] * mnq, nrmc[p], bic[p]);
-      fixrep_row<P>(ed, a, q0 + i, J0 + tid * P);
+      if (repm) rep_apply<P>(ed, repm, a, q0 + i, J0 + tid * P);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const V e = VT<V>::of(ed[p]);
@@ -860,7 +880,15 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     xfer[0 * 64 + 0 * 32 + warp] = cov[P - 2 >= 0 ? P - 2 : 0];
     xfer[0 * 64 + 1 * 32 + warp] = cov[P - 1];
   }
-  __syncthreads();
+  __shared__ unsigned rmap[REP_WORDS];
+  if (a.rep)
+    rep_build(rmap, a.hash, q0, w, tid, NT);  // ends with a barrier
+  else
+    __syncthreads();  // ends with a barrier
+  unsigned repm = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (a.rep && tid * P + p < NC && rep_probe(rmap, a.hash[J0 + tid * P + p])) repm |= 1u << p;
 
   const int qloc = (int)(q0 - J0) - tid * P;
   VHGeom g;
@@ -886,7 +914,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
       double ed[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) ed[p] = fma(cv[p] * mnq, nrmc[p], bic[p]);
-      fixrep_row<P>(ed, a, q0 + i, J0 + tid * P);
+      if (repm) rep_apply<P>(ed, repm, a, q0 + i, J0 + tid * P);
 #pragma unroll
       for (int p = 0; p < P; ++p) {
         const V e = VT<V>::of(ed[p]);
@@ -1119,7 +1147,15 @@ __global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPAr
     pos[p] = (j % R) * 32 + j / R;
   }
   const bool rem_ok = tid + D < NT;  // my windows' last columns exist in this tile
-  __syncthreads();
+  __shared__ unsigned rmap[REP_WORDS];
+  if (a.rep)
+    rep_build(rmap, a.hash, q0, w, tid, NT);  // ends with a barrier
+  else
+    __syncthreads();  // ends with a barrier
+  unsigned repm = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (a.rep && c0 + p < NC && rep_probe(rmap, a.hash[J0 + c0 + p])) repm |= 1u << p;
 
   for (int i = 0; i < w; ++i) {
     const int par = i & 1;
@@ -1144,7 +1180,7 @@ __global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPAr
 #pragma unroll
         for (int p = 0; p < P; ++p) ed[p] = fma(cov[p] * mnq, nrmc[p], (c0 + p < NC) ? a.bias[J0 + c0 + p] : PST_INF);
       }
-      fixrep_row<P>(ed, a, q0 + i, J0 + c0);
+      if (repm) rep_apply<P>(ed, repm, a, q0 + i, J0 + c0);
 #pragma unroll
       for (int p = 0; p < P; ++p) kk[p] = VT<V>::of(ed[p]);
     } else {  // constant query window (row-uniform branch): zdist.py:111-112
@@ -1648,7 +1684,7 @@ __global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
       if (i > 0) cur[u] = cvv;
       if (cl >= jl) {
         double e = (nq != 0.0) ? fma(cvv * (-nq), a.nrm[c], a.bias[c]) : a.cbias[c];
-        if (nq != 0.0 && __double2hiint(e) < KEY_E10) e = repeat_zero(e, a.x, a.hash, q, c, l);
+        if (nq != 0.0 && a.hash[q] == a.hash[c] && same_window(a.x, a.hash, q, c, l)) e = 0.0;
         if (c == q) e = 0.0;
         rm = vmin(rm, e);
         BAc[cl - jl] = vmin(BAc[cl - jl], e);  // column owned by this thread
@@ -2009,6 +2045,10 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   MPArgs a;
   a.x = c->x; a.mu = c->L.mc; a.nrm = c->L.nrm; a.bias = c->L.bias; a.cbias = c->L.cbias;
   a.df = c->L.df; a.dg = c->L.dg; a.hash = c->L.hash;
+  // exact-repeat rule: needed only when two windows share a hash (pst_ensure_len); PASTILA_REPEAT
+  // (test knob) forces it on (1) or off (0)
+  a.rep = c->L.has_rep ? 1 : 0;
+  if (const char* e = getenv("PASTILA_REPEAT")) a.rep = atoi(e) > 0;
   a.n = n; a.l = l; a.m = m; a.w = w; a.k = k; a.Nl = Nl; a.N = N; a.T = T;
   a.R = R; a.Tp = Tp;
   a.D = D_dev; a.ldD = ld;

@@ -2,6 +2,8 @@
 // selection, nearest-segment attribution, labels, Eq. 18 criterion, C-ABI.
 #include "common.cuh"
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -152,6 +154,11 @@ __global__ void k_hash(const double* __restrict__ x, int64_t n, int64_t l, unsig
   }
 }
 
+__global__ void k_adjacent_equal(const unsigned long long* __restrict__ v, int64_t n, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (v[i] == v[i + 1]) *flag = 1;
+}
+
 // Distance rows for queries q0..q0+rows-1 (zdist.py:191-225): one thread per
 // diagonal; diagonals entering at row 0 (column c0 >= 0) or at column 0
 // (row r0 > 0) start from a fresh centered dot product.
@@ -183,7 +190,7 @@ __global__ void k_rows(const double* __restrict__ x, LenData L, int64_t n, int64
       e = L.cbias[c];
     else
       e = fma(-(cov * nq), L.nrm[c], L.bias[c]);
-    if (e < 1e-10 && c != q && L.hash[q] == L.hash[c]) {  // exact repeat (bit-equal windows): d = 0
+    if (nq != 0.0 && c != q && L.hash[q] == L.hash[c]) {  // exact repeat (bit-equal windows): d = 0
       bool same = true;
       for (int64_t t = 0; t < l && same; ++t) same = __double_as_longlong(x[q + t]) == __double_as_longlong(x[c + t]);
       if (same) e = 0.0;
@@ -698,6 +705,24 @@ int pst_ensure_len(pst_ctx* c, int64_t l) {
   k_hash<<<grid_for(Nl, 256), 256, 0, c->st>>>(c->x, c->n, l, c->L.hash);
   c->launches += 3;
   PST_CUDA(cudaGetLastError());
+  {  // any two equal window hashes?  (sorted copy, adjacent compare); if none, no exact repeat exists
+    size_t tmp = 0;
+    PST_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const unsigned long long*)nullptr,
+                                            (unsigned long long*)nullptr, (int)Nl, 0, 64, c->st));
+    const size_t kb = ((size_t)Nl * 8 + 255) & ~(size_t)255;
+    PST_TRY(pst_ensure(&c->aux, &c->aux_bytes, kb + 256 + tmp));
+    unsigned long long* sorted = (unsigned long long*)c->aux;
+    int* flag = (int*)((char*)c->aux + kb);
+    void* tmpp = (char*)c->aux + kb + 256;
+    PST_CUDA(cub::DeviceRadixSort::SortKeys(tmpp, tmp, c->L.hash, sorted, (int)Nl, 0, 64, c->st));
+    PST_CUDA(cudaMemsetAsync(flag, 0, 4, c->st));
+    k_adjacent_equal<<<grid_for(Nl, 256), 256, 0, c->st>>>(sorted, Nl, flag);
+    c->launches += 2;
+    int h = 0;
+    PST_CUDA(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));
+    c->L.has_rep = h != 0;
+  }
   c->L.l = l;
   c->L.Nl = Nl;
   return PST_OK;
@@ -751,7 +776,8 @@ int pst_destroy(pst_ctx* c) {
   cudaSetDevice(c->dev);
   cudaStreamSynchronize(c->st);
   void* ptrs[] = {c->x, c->csum, c->csq, c->chg, c->L.mu, c->L.var, c->L.sd, c->L.nrm, c->L.bias,
-                  c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg, c->Dk, c->cert};
+                  c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg, c->Dk, c->cert,
+                  c->L.hash, c->aux};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st2) {
@@ -1623,6 +1649,7 @@ int pst_window_exact(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t*
       return PST_EINVAL;
     }
   if (cnt <= 0) return PST_OK;
+  PST_TRY(pst_ensure_len(c, l));  // before taking c->work: a new length rebuilds its arrays through it
   const size_t b = (size_t)cnt * 8;
   PST_TRY(pst_ensure(&c->work, &c->work_bytes, 3 * ((b + 255) & ~(size_t)255)));
   char* w = (char*)c->work;

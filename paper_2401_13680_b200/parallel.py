@@ -169,6 +169,9 @@ class DeviceRows:
         self.N = n - m + 1
         self.rows = seg_hi - seg_lo
         self.D = torch.empty((self.rows, self.N), dtype=torch.float64, device=self.dev)
+        if self.rows == 0:  # more ranks than segments: this rank owns none
+            return
+        torch.cuda.synchronize(self.dev)  # D allocated on torch's stream, written on the library's
         with self.ctx.using(series.values):
             self.ctx.call("pst_profiles_dev", int(m), int(params.window_size), int(params.k), int(seg_lo),
                           int(seg_hi), C.c_void_p(self.D.data_ptr()), C.c_int64(self.N))
@@ -178,10 +181,13 @@ class DeviceRows:
         import torch
 
         out = torch.empty(self.rows, dtype=torch.float64, device=self.dev)
+        if self.rows == 0:
+            return out.cpu().numpy()
         cptr = None
         if curve is not None:
             ct = torch.as_tensor(curve, dtype=torch.float64, device=self.dev)
             cptr = self.C.c_void_p(ct.data_ptr())
+        torch.cuda.synchronize(self.dev)  # inputs written on torch's stream
         self.ctx.call("pst_areas_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
                       self.C.c_int64(self.N), self.C.c_int64(self.N), cptr, self.C.c_void_p(out.data_ptr()))
         self.ctx.call("pst_sync")
@@ -193,6 +199,8 @@ class DeviceRows:
     def colmin(self):
         import torch
 
+        if self.rows == 0:
+            return np.full(self.N, np.inf), np.zeros(self.N, dtype=np.int64)
         mv = torch.empty(self.N, dtype=torch.float64, device=self.dev)
         ma = torch.empty(self.N, dtype=torch.int32, device=self.dev)
         self.ctx.call("pst_colmin_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
@@ -251,6 +259,7 @@ class StreamedRows:
             mat = torch.zeros(self.N, dtype=torch.int32, device=self.dev)
             mxt = torch.zeros(1, dtype=torch.float64, device=self.dev)
             mv, ma, mx = (C.c_void_p(t.data_ptr()) for t in (mvt, mat, mxt))
+        torch.cuda.synchronize(self.dev)  # filled on torch's stream, reduced on the library's
         with self.ctx.using(self.values):
             self.ctx.call("pst_profile_reduce_dev", *self._mkl(), self.lo, self.hi, cptr,
                           C.c_void_p(out.data_ptr()), mv, ma, mx)
@@ -309,7 +318,13 @@ def select_snippets_sharded(series, params, num_snippets: int, *, backend=None):
         backend = (DeviceRows if fits else StreamedRows)(series, params, lo, hi)
     d = _dist()
     on_gpu = d is not None and d.get_backend() == "nccl"
-    tdev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    if on_gpu:  # the collectives run on the GPU of this rank's library context
+        from . import _native
+
+        tdev = torch.device("cuda", _native.context().device)
+        torch.cuda.set_device(tdev)
+    else:
+        tdev = torch.device("cpu")
 
     def to_dev(a):
         return torch.as_tensor(np.ascontiguousarray(a)).to(tdev)
@@ -327,8 +342,35 @@ def select_snippets_sharded(series, params, num_snippets: int, *, backend=None):
     profiles = tuple(MPdistProfile(segment_index=int(chosen[r]), values=ss.chosen_rows[r]) for r in order)
     return SnippetResult(
         snippet_size=m, window_size=params.window_size, k=params.k, series_length=n, snippets=snippets,
-        curve=curve, profile_area=float(np.asarray(curve).sum()), profiles=profiles, profile_max=float(pmax),
+        curve=curve, profile_area=curve_area(curve), profiles=profiles, profile_max=float(pmax),
         segment_window_counts=counts, unassigned_windows=int(N - sum(counts[c] for c in chosen)))
+
+
+def curve_area(curve) -> float:
+    """profile_area with the same device reduction as the single-GPU search
+    (pst_areas_dev over one row: fixed-order block sum, pastila.cu k_areas), so
+    results are byte-identical across GPU counts; numpy's sum without a GPU."""
+    c = np.ascontiguousarray(curve, dtype=np.float64)
+    try:
+        import ctypes as C
+
+        import torch
+
+        from . import _native
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("no GPU")
+        ctx = _native.context()
+    except Exception:
+        return float(c.sum())
+    dev = torch.device("cuda", ctx.device)
+    ct = torch.as_tensor(c, device=dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    ctx.call("pst_areas_dev", C.c_void_p(ct.data_ptr()), C.c_int64(1), C.c_int64(c.size), C.c_int64(c.size),
+             None, C.c_void_p(out.data_ptr()))
+    ctx.call("pst_sync")
+    return float(out.item())
 
 
 def timed(fn, *a, **kw):

@@ -8,12 +8,15 @@ Reference behaviour: sniplab/cli.py:94-281 and the reference's test_cli.py.
 import json
 import subprocess
 import sys
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 from paper_2401_13680_b200 import cli
 from paper_2401_13680_b200.datagen import planted_walk
+
+ROOT = Path(__file__).resolve().parents[1]
 
 
 def _run(args, capsys):
@@ -103,3 +106,27 @@ class TestGPU:
         got = np.array([int(v) for v in out.split()])
         r = O.select_snippets(x, 32, 2)
         np.testing.assert_array_equal(got, O.labels(list(r["profiles"]), x.size))
+
+
+@pytest.mark.gpu
+def test_sweep_outputs_identical_across_workers(tmp_path):
+    """Reference acceptance #7 (pkg/tests/test_acceptance.py:181-222): the sweep's report
+    and snippet JSON are byte-identical for 1, 2 and 4 workers.  Workers are processes
+    bound to GPUs (run_schedule, KK partition of the lengths); here all share one GPU."""
+    from paper_2401_13680_b200.datagen import two_regime_series
+
+    x, _ = two_regime_series(n=20000, period=32, block_len=1024, noise=0.1, seed=7)
+    f = _series_csv(tmp_path, x)
+
+    def run(workers):
+        rep, snip = tmp_path / f"r{workers}.json", tmp_path / f"s{workers}.json"
+        argv = [sys.executable, "-m", "paper_2401_13680_b200", "sweep", "--input", f, "--m-min", "8",
+                "--m-max", "1024", "--k", "2", "--workers", str(workers), "--no-log",
+                "--output", str(rep), "--output-snippets", str(snip)]
+        proc = subprocess.run(argv, capture_output=True, text=True, timeout=900, cwd=str(ROOT))
+        assert proc.returncode == 0, proc.stderr
+        return rep.read_bytes() + snip.read_bytes()
+
+    solo = run(1)
+    assert run(2) == solo
+    assert run(4) == solo

@@ -508,18 +508,74 @@ __device__ __forceinline__ void store_ab_combine(const AbStore& g, const V* __re
 
 __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
+// ---- TMA bulk staging of a tile's series samples (cp.async.bulk + mbarrier) --
+// The row-0 and left-edge fresh dot products read the tile's column samples
+// x[J0 .. J0+NC+l-1) and the segment's samples x[q0 .. q0+m); one elected
+// thread copies both ranges global -> shared with 1-D bulk copies completing on
+// an mbarrier (16-byte granularity: the ranges are widened to 16-byte aligned
+// boundaries; the series buffer is padded, pastila.cu set_series).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+struct BulkStage {
+  const double* xt;  // tile samples: xt[t] = x[J0 + t]
+  const double* xq;  // segment samples: xq[t] = x[q0 + t]
+};
+// stage [J0, J0+nt) and [q0, q0+nq) into buf (doubles, 16-byte aligned, room for nt+nq+4); all threads
+// call it; returns views valid after the call (ends with the mbarrier wait)
+__device__ __forceinline__ BulkStage bulk_stage(double* buf, unsigned long long* mbar, const double* x, int64_t J0,
+                                                int nt, int64_t q0, int nq, int tid) {
+  const int64_t a0 = J0 & ~1ll, a1 = q0 & ~1ll;                     // 16-byte aligned starts
+  const int n0 = (int)(((J0 + nt) - a0 + 1) & ~1), n1 = (int)(((q0 + nq) - a1 + 1) & ~1);  // even counts
+  double* b0 = buf;
+  double* b1 = buf + n0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned bytes = (unsigned)(n0 + n1) * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(b0)),
+        "l"(x + a0), "r"((unsigned)n0 * 8u), "r"(smem_u32(mbar))
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(b1)),
+        "l"(x + a1), "r"((unsigned)n1 * 8u), "r"(smem_u32(mbar))
+        : "memory");
+  }
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(mbar))
+        : "memory");
+  }
+  BulkStage st;
+  st.xt = b0 + (J0 - a0);
+  st.xq = b1 + (q0 - a1);
+  return st;
+}
+__host__ __device__ inline size_t bulk_bytes(int64_t ncmax, int64_t l, int64_t m) {
+  return (size_t)(ncmax + l + m + 8) * 8 + 16;  // both ranges + alignment slack + mbarrier
+}
+
 // Dynamic shared memory of the one-row kernel (k_mpdist): doubles first
 // (row-0 staging xs[l], left-edge dots, per-row scalars, warp exchange), then
 // the V arrays (e rows, AB row buffers; long windows: split van Herk buffers).
 __host__ __device__ inline size_t smem_row1(bool klong, int64_t l, int64_t w, int64_t ncm, size_t sv) {
-  if (!klong) return align16((size_t)(l + 4 * w + 66) * 8) + (size_t)(4 * ncm) * sv;
+  if (!klong) return align16(align16((size_t)(l + 4 * w + 66) * 8) + (size_t)(4 * ncm) * sv) + bulk_bytes(ncm, l, l + w - 1);
   size_t b = align16((size_t)(w + 66) * 8) + (size_t)(6 * ncm + 1024) * sv;
   if ((size_t)l * 8 > (size_t)ncm * sv) b = align16(b) + (size_t)l * 8;  // xs does not fit E1
   return b;
 }
 // two rows per barrier (k_mpdist2)
 __host__ __device__ inline size_t smem_row2(int64_t l, int64_t w, int64_t ncm, size_t sv) {
-  return align16((size_t)(l + 4 * w + 130) * 8) + (size_t)(8 * ncm) * sv;
+  return align16(align16((size_t)(l + 4 * w + 130) * 8) + (size_t)(8 * ncm) * sv) + bulk_bytes(ncm, l, l + w - 1);
 }
 
 template <int P, int NT, int CHM, class V>
@@ -575,6 +631,13 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   const double* __restrict__ xQ = a.x + q0;
   const double* __restrict__ muJ = a.mu + J0;
   const double* __restrict__ muQ = a.mu + q0;
+  if constexpr (!kLong) {  // samples of the fresh dots staged in shared memory by TMA bulk copies
+    double* buf = (double*)align16((size_t)(SR1 + NCmax));
+    const BulkStage st = bulk_stage(buf, (unsigned long long*)(buf + NCmax + l + a.m + 8), a.x, J0, NC + l - 1,
+                                    q0, (int)a.m, tid);
+    xJ = st.xt;
+    xQ = st.xq;
+  }
 
   // ---- row-0 fresh dots: cov(q0, c) = sum_t (x[q0+t]-mu[q0]) x[c+t] - mu[c] sum_t (x[q0+t]-mu[q0])
   {
@@ -798,10 +861,14 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   V* SRB = EB + 4 * NCmax;       // [4][NCmax] AB row buffers
   const int R = (int)a.R, Tp = (int)a.Tp;
   V* ab = (V*)a.ab + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * ((int64_t)w * Tp);
-  const double* __restrict__ xJ = a.x + J0;
-  const double* __restrict__ xQ = a.x + q0;
   const double* __restrict__ muJ = a.mu + J0;
   const double* __restrict__ muQ = a.mu + q0;
+  // samples of the fresh dots staged in shared memory by TMA bulk copies
+  double* sbuf = (double*)align16((size_t)(SRB + 4 * NCmax));
+  const BulkStage stg = bulk_stage(sbuf, (unsigned long long*)(sbuf + NCmax + l + a.m + 8), a.x, J0, NC + l - 1,
+                                   q0, (int)a.m, tid);
+  const double* __restrict__ xJ = stg.xt;
+  const double* __restrict__ xQ = stg.xq;
 
   // ---- row-0 fresh dots (as k_mpdist)
   {

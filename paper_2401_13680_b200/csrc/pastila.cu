@@ -808,7 +808,7 @@ static int set_series_common(pst_ctx* c, const double* x, int64_t n, cudaMemcpyK
     }
     c->cap_n = 0;
     size_t cap = 0;
-    PST_TRY(pst_ensure((void**)&c->x, &cap, (size_t)n * sizeof(double)));
+    PST_TRY(pst_ensure((void**)&c->x, &cap, (size_t)(n + 8) * sizeof(double)));  // padded: 16-byte bulk copies
     cap = 0;
     PST_TRY(pst_ensure((void**)&c->csum, &cap, (size_t)(n + 1) * sizeof(double)));
     cap = 0;

@@ -122,6 +122,9 @@ int pst_areas_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, in
  * argmin_dev [N].                                                          */
 int pst_colmin_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld,
                    int64_t row_base, double* minval_dev, int32_t* argmin_dev);
+/* Max over a rows x N device matrix (profile_max of a rank's segment rows,
+ * snippets.py:241); out_dev receives one double.                          */
+int pst_max_dev(pst_ctx* ctx, const double* D_dev, int64_t rows, int64_t N, int64_t ld, double* out_dev);
 /* Profiles of segments [seg_lo, seg_hi) computed in device-sized chunks and
  * reduced without being stored (S x N larger than HBM, C4: n = 1e7):
  * areas_dev[s-seg_lo] = sum_j min(D[s][j], curve_dev[j]) (curve NULL: +inf);
@@ -150,6 +153,30 @@ int pst_window_exact(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, const int64_
  * candidate, uncertain attribution windows, exact window evaluations,
  * profile_max candidates, fallbacks to the exact path, windows].         */
 int pst_cert_stats(pst_ctx* ctx, int64_t* out8, int reset);
+/* ---- multi-GPU data plane (segment-row sharding; the
+ * reference has none: its workers are processes, scheduler.py:373-405) ----
+ * One NCCL communicator per context (NCCL is dlopen'ed).  Rank 0 creates the
+ * 128-byte id, the caller distributes it, every rank calls pst_comm_init.
+ * Collectives are in place on device buffers on the context stream:
+ * dtype 0 = f64, 1 = i64, 2 = i32; op 0 = min, 1 = max, 2 = sum.          */
+int pst_comm_unique_id(char* out128);
+int pst_comm_init(pst_ctx* ctx, const char* id128, int nranks, int rank);
+int pst_comm_destroy(pst_ctx* ctx);
+int pst_comm_allreduce(pst_ctx* ctx, void* buf_dev, int64_t count, int dtype, int op);
+int pst_comm_broadcast(pst_ctx* ctx, void* buf_dev, int64_t bytes, int root);
+int pst_comm_allgather(pst_ctx* ctx, const void* send_dev, void* recv_dev, int64_t bytes_per_rank);
+/* Device glue of the sharded greedy (snippets.py:201-213 split over ranks):
+ * best available local row as (area, global index) [2 doubles]; global pick
+ * among nranks gathered pairs (marks it taken if local); attribution tie
+ * indices idx[j] = local_arg[j] + base where the local minimum equals the
+ * global one, else INT64_MAX; curve = row (first) or min(curve, row).     */
+int pst_local_best_dev(pst_ctx* ctx, const double* areas_dev, const uint8_t* taken_dev, int64_t rows,
+                       int64_t base, double* out2_dev);
+int pst_pick_global_dev(pst_ctx* ctx, const double* pairs_dev, int nranks, int64_t base, int64_t rows,
+                        uint8_t* taken_dev, double* out2_dev);
+int pst_tie_index_dev(pst_ctx* ctx, const double* lmin_dev, const double* gmin_dev, const int32_t* larg_dev,
+                      int64_t base, int64_t N, int64_t* out_dev);
+int pst_curve_min_dev(pst_ctx* ctx, double* curve_dev, const double* row_dev, int64_t N, int first);
 /* Instrumentation: milliseconds of the profile row-loop and selection
  * kernels since the last call (needs PASTILA_KTIME=1 and pst_timing on).  */
 int pst_kernel_times(pst_ctx* ctx, double* out2);

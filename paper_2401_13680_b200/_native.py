@@ -42,6 +42,7 @@ SIGNATURES = {
     "pst_destroy": (C.c_int, [_vp]),
     "pst_last_error": (C.c_char_p, []),
     "pst_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "pst_comm_unique_id": (C.c_int, [C.c_char_p]),
     "pst_set_series": (C.c_int, [_vp, _dp, _i64]),
     "pst_set_series_dev": (C.c_int, [_vp, _vp, _i64]),
     "pst_sliding_stats": (C.c_int, [_vp, _i64, _dp, _dp, _dp]),
@@ -52,6 +53,7 @@ SIGNATURES = {
     "pst_profiles_dev": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64]),
     "pst_areas_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _vp]),
     "pst_colmin_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "pst_max_dev": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "pst_profile_reduce_dev": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pst_sweep": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "pst_criterion": (C.c_int, [_vp, _dp, _i64, _i64, C.c_double, _dp]),
@@ -60,6 +62,15 @@ SIGNATURES = {
     "pst_window_exact": (C.c_int, [_vp, _i64, _i64, _i64, _lp, _lp, _i64, _dp]),
     "pst_cert_stats": (C.c_int, [_vp, _lp, C.c_int]),
     "pst_kernel_times": (C.c_int, [_vp, _dp]),
+    "pst_comm_init": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
+    "pst_comm_destroy": (C.c_int, [_vp]),
+    "pst_comm_allreduce": (C.c_int, [_vp, _vp, _i64, C.c_int, C.c_int]),
+    "pst_comm_broadcast": (C.c_int, [_vp, _vp, _i64, C.c_int]),
+    "pst_comm_allgather": (C.c_int, [_vp, _vp, _vp, _i64]),
+    "pst_local_best_dev": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp]),
+    "pst_pick_global_dev": (C.c_int, [_vp, _vp, C.c_int, _i64, _i64, _vp, _vp]),
+    "pst_tie_index_dev": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    "pst_curve_min_dev": (C.c_int, [_vp, _vp, _vp, _i64, C.c_int]),
     "pst_debug_hist": (C.c_int, [_vp, _lp]),
     "pst_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "pst_timing": (C.c_int, [_vp, C.c_int]),

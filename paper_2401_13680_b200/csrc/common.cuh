@@ -98,6 +98,9 @@ struct pst_ctx {
   double k_ms[2] = {0.0, 0.0};
   int num_sms = 148;
   size_t smem_optin = 0;
+  // NCCL communicator of the sharded search (comm.cu), one per context
+  void* comm = nullptr;
+  int comm_size = 1, comm_rank = 0;
 };
 
 int pst_ensure(void** p, size_t* cap, size_t bytes);

@@ -775,6 +775,7 @@ int pst_destroy(pst_ctx* c) {
   if (!c) return PST_OK;
   cudaSetDevice(c->dev);
   cudaStreamSynchronize(c->st);
+  pst_comm_destroy(c);
   void* ptrs[] = {c->x, c->csum, c->csq, c->chg, c->L.mu, c->L.var, c->L.sd, c->L.nrm, c->L.bias,
                   c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg, c->Dk, c->cert,
                   c->L.hash, c->aux};
@@ -943,6 +944,19 @@ int pst_areas_dev(pst_ctx* c, const double* D, int64_t rows, int64_t N, int64_t 
   k_areas<<<(unsigned)rows, 256, 0, c->st>>>(D, N, ld, curve, areas);
   c->launches++;
   PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+
+// max over rows x N of a device matrix (profile_max of a rank's rows, snippets.py:241); out_dev: 1 double
+int pst_max_dev(pst_ctx* c, const double* D, int64_t rows, int64_t N, int64_t ld, double* out_dev) {
+  if (!valid(c)) return PST_EINVAL;
+  PST_CUDA(cudaMemsetAsync(out_dev, 0, 8, c->st));
+  if (rows > 0) {
+    dim3 g((unsigned)grid_for(N, 256, 64), (unsigned)std::min<int64_t>(rows, 64));
+    k_max<<<g, 256, 0, c->st>>>(D, rows, N, ld, (unsigned long long*)out_dev);
+    c->launches++;
+    PST_CUDA(cudaGetLastError());
+  }
   return PST_OK;
 }
 

@@ -196,6 +196,33 @@ class DeviceRows:
     def row(self, i):
         return self.D[i].cpu().numpy()
 
+    # device-resident variants for the library NCCL path (DeviceShardedSearch)
+    def areas_dev(self, curve_t):
+        import torch
+
+        out = torch.empty(self.rows, dtype=torch.float64, device=self.dev)
+        if self.rows:
+            cptr = self.C.c_void_p(curve_t.data_ptr()) if curve_t is not None else None
+            self.ctx.call("pst_areas_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
+                          self.C.c_int64(self.N), self.C.c_int64(self.N), cptr, self.C.c_void_p(out.data_ptr()))
+        return out
+
+    def row_dev(self, i):
+        return self.D[i]
+
+    def colmin_dev(self):
+        import torch
+
+        mv = torch.full((self.N,), float("inf"), dtype=torch.float64, device=self.dev)
+        ma = torch.zeros(self.N, dtype=torch.int32, device=self.dev)
+        torch.cuda.synchronize(self.dev)
+        if self.rows:
+            self.ctx.call("pst_colmin_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
+                          self.C.c_int64(self.N), self.C.c_int64(self.N), self.C.c_int64(0),
+                          self.C.c_void_p(mv.data_ptr()), self.C.c_void_p(ma.data_ptr()))
+            self.ctx.call("pst_sync")  # the caller may touch them on torch's stream
+        return mv, ma
+
     def colmin(self):
         import torch
 
@@ -210,7 +237,15 @@ class DeviceRows:
         return mv.cpu().numpy(), ma.cpu().numpy().astype(np.int64)
 
     def rowmax(self):
-        return float(self.D.max().item()) if self.rows else 0.0
+        import torch
+
+        if not self.rows:
+            return 0.0
+        out = torch.empty(1, dtype=torch.float64, device=self.dev)
+        self.ctx.call("pst_max_dev", self.C.c_void_p(self.D.data_ptr()), self.C.c_int64(self.rows),
+                      self.C.c_int64(self.N), self.C.c_int64(self.N), self.C.c_void_p(out.data_ptr()))
+        self.ctx.call("pst_sync")
+        return float(out.item())
 
 
 class StreamedRows:
@@ -289,8 +324,133 @@ class StreamedRows:
             self.areas(None)
         return self._rowmax if self.rows else 0.0
 
+    # device-resident variants for the library NCCL path (DeviceShardedSearch)
+    def areas_dev(self, curve_t):
+        torch = self.torch
+        curve = None if curve_t is None else curve_t.cpu().numpy()
+        return torch.as_tensor(self.areas(curve), device=self.dev)
 
-def select_snippets_sharded(series, params, num_snippets: int, *, backend=None):
+    def row_dev(self, i):
+        return self.torch.as_tensor(self.row(i), device=self.dev)
+
+    def colmin_dev(self):
+        mv, ma = self.colmin()
+        torch = self.torch
+        return (torch.as_tensor(mv, dtype=torch.float64, device=self.dev),
+                torch.as_tensor(ma, dtype=torch.int32, device=self.dev))
+
+
+class LibComm:
+    """NCCL communicator owned by libpastila (csrc/comm.cu, pst_comm_*): the
+    collectives of the sharded search run inside the library, on its stream,
+    on device buffers.  Bootstrap only goes through torch.distributed: rank 0's
+    128-byte ncclUniqueId is broadcast as an object.  One per context."""
+
+    _by_ctx: dict = {}
+
+    def __init__(self):
+        import ctypes as C
+
+        from . import _native
+
+        self.C, self.ctx = C, _native.context()
+        self.ws, self.rk = world_size(), rank()
+        uid = C.create_string_buffer(128)
+        if self.rk == 0:
+            _native._check(_native.load_library().pst_comm_unique_id(uid), "pst_comm_unique_id")
+        raw = uid.raw
+        if self.ws > 1:
+            obj = [raw]
+            _dist().broadcast_object_list(obj, src=0)
+            raw = obj[0]
+        self.ctx.call("pst_comm_init", raw, self.ws, self.rk)
+
+    @classmethod
+    def get(cls):
+        from . import _native
+
+        key = (id(_native.context()), world_size(), rank())
+        c = cls._by_ctx.get(key)
+        if c is None:
+            c = cls._by_ctx[key] = cls()
+        return c
+
+    def p(self, t):
+        return self.C.c_void_p(t.data_ptr())
+
+    def all_gather(self, send, recv):
+        self.ctx.call("pst_comm_allgather", self.p(send), self.p(recv), send.numel() * send.element_size())
+
+    def broadcast(self, t, root):
+        self.ctx.call("pst_comm_broadcast", self.p(t), t.numel() * t.element_size(), int(root))
+
+    def all_reduce(self, t, op):  # op: "min" | "max"
+        import torch
+
+        dtype = {torch.float64: 0, torch.int64: 1, torch.int32: 2}[t.dtype]
+        self.ctx.call("pst_comm_allreduce", self.p(t), t.numel(), dtype, {"min": 0, "max": 1, "sum": 2}[op])
+
+
+class DeviceShardedSearch:
+    """ShardedSearch with every per-step and per-window quantity on the device:
+    local best (pst_local_best_dev), all-gather of the (area, index) pairs and the
+    global pick (pst_pick_global_dev), broadcast of the chosen profile from its
+    owner, curve update (pst_curve_min_dev), attribution by all-reduce MIN of the
+    minima then of the tie indices (pst_tie_index_dev), profile_max by all-reduce
+    MAX -- all through LibComm.  Host traffic: one 16-byte pick per step and the
+    final outputs."""
+
+    def __init__(self, backend, ranges, N: int, comm: LibComm):
+        self.b, self.ranges, self.N, self.comm = backend, list(ranges), N, comm
+        self.lo, self.hi = self.ranges[comm.rk]
+
+    def run(self, K: int):
+        import torch
+
+        C, ctx, comm = self.comm.C, self.comm.ctx, self.comm
+        dev = torch.device("cuda", ctx.device)
+        rows, N, ws = self.hi - self.lo, self.N, comm.ws
+        taken = torch.zeros(max(rows, 1), dtype=torch.uint8, device=dev)
+        pair = torch.tensor([float("inf"), 9.0e18], dtype=torch.float64, device=dev)
+        pairs = torch.empty(2 * ws, dtype=torch.float64, device=dev)
+        pick = torch.empty(2, dtype=torch.float64, device=dev)
+        curve = torch.empty(N, dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)  # torch-filled buffers, library stream from here on
+        chosen, self.chosen_rows = [], []
+        for step in range(K):
+            areas = self.b.areas_dev(curve if step else None)
+            if rows:
+                ctx.call("pst_local_best_dev", comm.p(areas), comm.p(taken), rows, self.lo, comm.p(pair))
+            comm.all_gather(pair, pairs)
+            ctx.call("pst_pick_global_dev", comm.p(pairs), ws, self.lo, rows, comm.p(taken), comm.p(pick))
+            ctx.call("pst_sync")
+            gi = int(pick[1].item())
+            chosen.append(gi)
+            owner = next(r for r, (lo, hi) in enumerate(self.ranges) if lo <= gi < hi)
+            if owner == comm.rk:
+                row = self.b.row_dev(gi - self.lo).contiguous()
+            else:
+                row = torch.empty(N, dtype=torch.float64, device=dev)
+            torch.cuda.synchronize(dev)
+            comm.broadcast(row, owner)
+            ctx.call("pst_curve_min_dev", comm.p(curve), comm.p(row), N, 1 if step == 0 else 0)
+            self.chosen_rows.append(row)
+        mv, ma = self.b.colmin_dev()
+        gmin = mv.clone()
+        torch.cuda.synchronize(dev)
+        comm.all_reduce(gmin, "min")
+        idx = torch.empty(N, dtype=torch.int64, device=dev)
+        ctx.call("pst_tie_index_dev", comm.p(mv), comm.p(gmin), comm.p(ma), self.lo, N, comm.p(idx))
+        comm.all_reduce(idx, "min")
+        pm = torch.tensor([self.b.rowmax()], dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)
+        comm.all_reduce(pm, "max")
+        ctx.call("pst_sync")
+        self.chosen_rows = [r.cpu().numpy() for r in self.chosen_rows]
+        return chosen, curve.cpu().numpy(), idx.cpu().numpy(), float(pm.item())
+
+
+def select_snippets_sharded(series, params, num_snippets: int, *, backend=None, comm=None):
     """``select_snippets`` for ONE length with its segment rows sharded over the
     ranks of the default process group: rank r owns a
     contiguous segment range, keeps its profiles in HBM when they fit
@@ -332,7 +492,14 @@ def select_snippets_sharded(series, params, num_snippets: int, *, backend=None):
     def from_dev(t):
         return t.cpu().numpy()
 
-    ss = ShardedSearch(backend, ranges, N, to_dev, from_dev)
+    if comm is None:  # default: the library's NCCL on GPUs; PASTILA_COMM=torch selects torch.distributed (A/B)
+        import os
+
+        comm = os.environ.get("PASTILA_COMM", "lib" if on_gpu else "torch")
+    if comm == "lib":  # library-owned NCCL data plane
+        ss = DeviceShardedSearch(backend, ranges, N, LibComm.get())
+    else:  # torch.distributed collectives (gloo CPU tests)
+        ss = ShardedSearch(backend, ranges, N, to_dev, from_dev)
     chosen, curve, nearest, pmax = ss.run(K)
     counts = np.bincount(nearest, minlength=S).astype(np.int64)
     order = sorted(range(K), key=lambda r: (-(counts[chosen[r]] / N), chosen[r]))  # snippets.py:228

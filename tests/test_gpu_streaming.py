@@ -152,3 +152,19 @@ def test_two_ranks_row_sharded_on_device(series, backend):
     np.testing.assert_array_equal(prof, np.vstack([p_.values for p_ in ref.profiles]))
     assert pmax == ref.profile_max
     np.testing.assert_array_equal(counts, ref.segment_window_counts)
+
+
+@pytest.mark.parametrize("backend", ["DeviceRows", "StreamedRows"])
+def test_library_nccl_sharded_search_equals_resident(series, monkeypatch, backend):
+    """The library-owned NCCL data plane (csrc/comm.cu: pst_comm_* collectives and the
+    device glue kernels, DeviceShardedSearch) in a single-rank communicator: every
+    collective, the on-device pick and the tie-index attribution run, and the result
+    is byte-identical to the resident single-GPU search."""
+    s, p = P.TimeSeries(series), P.MPdistParams(120)
+    resident = P.select_snippets(s, p, 3)
+    monkeypatch.setenv("PASTILA_STREAM_ROWS", "5")
+    S = series.size // 120
+    b = getattr(parallel, backend)(s, p, 0, S)
+    got = parallel.select_snippets_sharded(s, p, 3, backend=b, comm="lib")
+    _same(resident, got)
+    assert got.profile_area == resident.profile_area

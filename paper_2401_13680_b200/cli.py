@@ -60,7 +60,68 @@ def _validate(ns) -> None:
         raise UsageError(f"--k must be at least 1, got {ns.k}")
 
 
+def _columns(ns) -> list[int] | None:
+    """--columns: multi-coordinate series (d > 1, Eq. 2) as the independent
+    per-coordinate loop the reference prescribes (series.py:87-144):
+    'all' or a comma list of zero-based CSV columns; None = single --column run."""
+    spec = getattr(ns, "columns", None)
+    if not spec:
+        return None
+    if spec == "all":
+        import csv
+
+        with open(ns.input, newline="") as fh:
+            for row in csv.reader(fh):
+                if row and any(cell.strip() for cell in row):
+                    return list(range(len(row)))
+        raise ValueError(f"series file {ns.input} has no rows")
+    try:
+        cols = [int(v) for v in spec.split(",")]
+    except ValueError:
+        raise UsageError(f"--columns must be 'all' or a comma list of column indices, got {spec!r}") from None
+    if len(set(cols)) != len(cols) or min(cols) < 0:
+        raise UsageError(f"--columns must list distinct non-negative indices, got {spec!r}")
+    return cols
+
+
+def _per_column(ns, run_one) -> int:
+    """Run one subcommand per coordinate; JSON documents are collected as
+    {"schema": 1, "coordinates": [{"column": c, ...}, ...]}, exports get a .c<col> suffix."""
+    cols = _columns(ns)
+    docs, extra = [], []
+    out, out_snip = ns.output, getattr(ns, "output_snippets", None)
+    exp = (getattr(ns, "export_curve", None), getattr(ns, "export_profiles", None))
+    for c in cols:
+        ns.column = c
+        if exp[0]:
+            ns.export_curve = f"{exp[0]}.c{c}"
+        if exp[1]:
+            ns.export_profiles = f"{exp[1]}.c{c}"
+        d, e = run_one(ns)
+        docs.append({"column": c, **d})
+        if e is not None:
+            extra.append({"column": c, **e})
+    _write_json({"schema": 1, "coordinates": docs}, out)
+    if out_snip:
+        _write_json({"schema": 1, "coordinates": extra}, out_snip)
+    return 0
+
+
 def run_discover(ns) -> int:
+    if _columns(ns) is not None:
+        from .series import load_series
+        from .snippets import select_snippets
+
+        def one(ns):
+            result = select_snippets(load_series(ns.input, column=ns.column), _params(ns), ns.k)
+            _exports(result, ns)
+            return result.to_dict(), None
+
+        return _per_column(ns, one)
+    return _run_discover_one(ns)
+
+
+def _run_discover_one(ns) -> int:
     from .series import load_series
     from .snippets import select_snippets
 
@@ -86,6 +147,13 @@ def _cost_model_from_log(path: str | None, n: int, enabled: bool):
 
 
 def run_sweep(ns) -> int:
+    if _columns(ns) is not None:
+        return _per_column(ns, _sweep_one)
+    report, best = _sweep_one(ns, write=True)
+    return 0
+
+
+def _sweep_one(ns, write: bool = False):
     from .length_select import make_grid, select_length
     from .scheduler import TRAINING_LOG_ENV
     from .series import load_series
@@ -101,18 +169,35 @@ def run_sweep(ns) -> int:
     report, results = select_length(series, grid, ns.k, window_rule=window_rule, workers=ns.workers,
                                     cost_model=_cost_model_from_log(log, series.n, not ns.no_log),
                                     training_log=False if ns.no_log else log)
-    _write_json(report.to_dict(), ns.output)
     best = results[report.m_best]
-    if ns.output_snippets:
-        _write_json(best.to_dict(), ns.output_snippets)
     _exports(best, ns)
-    return 0
+    if write:
+        _write_json(report.to_dict(), ns.output)
+        if ns.output_snippets:
+            _write_json(best.to_dict(), ns.output_snippets)
+    return report.to_dict(), best.to_dict()
 
 
 def run_label(ns) -> int:
     from .labeling import label_series, write_labels
     from .series import load_series
     from .snippets import select_snippets
+
+    cols = _columns(ns)
+    if cols is not None:  # one label column per coordinate
+        import numpy as np
+
+        lab = []
+        for c in cols:
+            ns.column = c
+            lab.append(label_series(select_snippets(load_series(ns.input, column=c), _params(ns), ns.k)).labels)
+        text = "".join(",".join(str(int(v)) for v in row) + "\n" for row in np.column_stack(lab))
+        if ns.output is not None:
+            with open(ns.output, "w") as fh:
+                fh.write(text)
+        else:
+            sys.stdout.write(text)
+        return 0
 
     labels = label_series(select_snippets(load_series(ns.input, column=ns.column), _params(ns), ns.k))
     if ns.output is not None:
@@ -131,7 +216,9 @@ def run_eval(ns) -> int:
 
 # (flags, kwargs) groups shared by the subcommands
 _INPUT = [(("--input",), dict(required=True, help="series CSV, one value per line")),
-          (("--column",), dict(type=int, default=0, help="CSV column to read"))]
+          (("--column",), dict(type=int, default=0, help="CSV column to read")),
+          (("--columns",), dict(default=None, help="multi-coordinate series: 'all' or a comma list of columns, "
+                                                   "each processed independently (overrides --column)"))]
 _FIXED_M = [(("--m",), dict(type=int, required=True, dest="m", help="snippet length")),
             (("--l",), dict(type=int, default=None, dest="l",
                             help="inner window length (default: half of --m, rounded up)")),

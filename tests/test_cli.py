@@ -130,3 +130,40 @@ def test_sweep_outputs_identical_across_workers(tmp_path):
     solo = run(1)
     assert run(2) == solo
     assert run(4) == solo
+
+
+def test_columns_usage_errors(capsys, tmp_path):
+    f = _series_csv(tmp_path, np.arange(50.0))
+    for bad in ("0,x", "1,1", "-1"):
+        rc, out, err = _run(["discover", "--input", f, "--m", "8", "--columns", bad], capsys)
+        assert rc == 2, (bad, err)
+
+
+@pytest.mark.gpu
+def test_multi_coordinate_loop_matches_single_columns(capsys, tmp_path):
+    """d > 1 (Eq. 2) as the independent per-coordinate loop of SPEC.md:13: --columns runs each
+    column exactly as --column would."""
+    cols = [planted_walk(3000, m_act=40, A=2, seed=s)[0] for s in (1, 2, 3)]
+    f = tmp_path / "multi.csv"
+    np.savetxt(f, np.column_stack(cols), fmt="%.17g", delimiter=",")
+    f = str(f)
+    rc, out, err = _run(["discover", "--input", f, "--m", "32", "--k", "2", "--columns", "all"], capsys)
+    assert rc == 0, err
+    multi = json.loads(out)
+    assert [d["column"] for d in multi["coordinates"]] == [0, 1, 2]
+    for c in range(3):
+        rc, out, err = _run(["discover", "--input", f, "--m", "32", "--k", "2", "--column", str(c)], capsys)
+        one = json.loads(out)
+        assert {k: v for k, v in multi["coordinates"][c].items() if k != "column"} == one
+    rc, out, err = _run(["label", "--input", f, "--m", "32", "--k", "2", "--columns", "0,2"], capsys)
+    assert rc == 0, err
+    lab = np.array([[int(v) for v in ln.split(",")] for ln in out.split()])
+    for j, c in enumerate((0, 2)):
+        rc, o1, _ = _run(["label", "--input", f, "--m", "32", "--k", "2", "--column", str(c)], capsys)
+        np.testing.assert_array_equal(lab[:, j], [int(v) for v in o1.split()])
+    rc, out, err = _run(["sweep", "--input", f, "--m-min", "16", "--m-max", "64", "--k", "2", "--no-log",
+                         "--columns", "1"], capsys)
+    assert rc == 0, err
+    rc, o1, _ = _run(["sweep", "--input", f, "--m-min", "16", "--m-max", "64", "--k", "2", "--no-log",
+                      "--column", "1"], capsys)
+    assert {k: v for k, v in json.loads(out)["coordinates"][0].items() if k != "column"} == json.loads(o1)

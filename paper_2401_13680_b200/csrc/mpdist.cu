@@ -1963,8 +1963,9 @@ int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& G) {
   int P = 5;
   // register van Herk for w <= 32*9; chunk width class
   // columns per lane in the register van Herk (measured best on B200, tools/tune.py)
-  int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 56) ? 7 : (w <= 72) ? 5 : (w <= 112) ? 7 : (w <= 128) ? 9
-          : (w <= 160) ? 5 : (w <= 224) ? 7 : (w <= 288) ? 9 : 0;
+  // (re-measured for the key path, tools/tune_keys.py, profiles/r02_tune_geometry.json)
+  int chm = (w <= 24) ? 3 : (w <= 40) ? 5 : (w <= 56) ? 7 : (w <= 72) ? 9 : (w <= 112) ? 7 : (w <= 160) ? 9
+          : (w <= 224) ? 7 : (w <= 288) ? 9 : 0;
   if (const char* e = getenv("PASTILA_CHM")) {  // tuning experiments
     const int v = atoi(e);
     if ((v == 3 || v == 5 || v == 7 || v == 9) && 32 * v >= w) chm = v;
@@ -2005,14 +2006,10 @@ int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& G) {
   G.smem_d = smem_for(P);
   // two rows per barrier (k_mpdist2): register van Herk, P = 5; used when one row
   // leaves lane-group slots idle and two rows fit one round
+  // two rows per barrier whenever it fits: measured +3-10% for w > 72 on the key path
   G.rows2 = false;
   if (chm > 0 && P == 5 && smem_row2(l, w, NCmax, 8) <= smax && nt != 128) {
-    int lpb = 1;
-    while (lpb < 32 && lpb * chm < w) lpb *= 2;
-    if (lpb < 8) lpb = 8;
-    const int64_t slots = (int64_t)(nt / 32) * (32 / lpb);
-    const int64_t nblk = (std::min(T, N) + w - 1) / w;
-    G.rows2 = 2 * nblk <= slots;
+    G.rows2 = true;
     if (const char* e = getenv("PASTILA_ROWS2")) G.rows2 = atoi(e) > 0;  // tuning experiments
   }
   return PST_OK;

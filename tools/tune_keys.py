@@ -27,11 +27,15 @@ for cfg in cfgs:
     try:
         with ctx.using(x):
             ctx.call("pst_profile_keys", m, pr.window_size, pr.k, 0, nseg, _native.ptr(out, C.c_int32))
-            ctx.call("pst_timing", 1)
-            ctx.call("pst_profile_keys", m, pr.window_size, pr.k, 0, nseg, _native.ptr(out, C.c_int32))
-            kms, kl = C.c_double(0), C.c_int64(0)
-            ctx.call("pst_timing_read", C.byref(kms), C.byref(kl))
-            ctx.call("pst_timing", 0)
+            best = None
+            for _ in range(int(os.environ.get("TUNE_REPS", "2"))):
+                ctx.call("pst_timing", 1)
+                ctx.call("pst_profile_keys", m, pr.window_size, pr.k, 0, nseg, _native.ptr(out, C.c_int32))
+                kms, kl = C.c_double(0), C.c_int64(0)
+                ctx.call("pst_timing_read", C.byref(kms), C.byref(kl))
+                ctx.call("pst_timing", 0)
+                best = kms.value if best is None else min(best, kms.value)
+            kms = C.c_double(best)
         l = pr.window_size
         pairs = (m - l + 1) * (x.size - l + 1) * nseg
         print(json.dumps({"m": m, "cfg": cfg, "ms": kms.value, "pairs_per_s": pairs / (kms.value / 1e3)}), flush=True)

@@ -578,6 +578,34 @@ __host__ __device__ inline size_t smem_row2(int64_t l, int64_t w, int64_t ncm, s
   return align16(align16((size_t)(l + 4 * w + 130) * 8) + (size_t)(8 * ncm) * sv) + bulk_bytes(ncm, l, l + w - 1);
 }
 
+// Row-0 fresh dots of a thread's P consecutive columns c0..c0+P-1:
+//   cov[p] = fma(-mu[c], sum xs, sum_t fma(xs[t], x[c+t], .))   (t sequential per column)
+// with the P chains interleaved and the x window sliding through registers
+// (one new sample per step).  Same per-column operation order as a plain loop.
+template <int P>
+__device__ __forceinline__ void row0_dots(double (&cov)[P], const double* __restrict__ xs,
+                                          const double* __restrict__ xJ, const double* __restrict__ muJ, double sx,
+                                          int c0, int NC, int l) {
+  double xw[P];
+  const int lim = NC + l - 1;  // samples x[J0 + 0 .. J0 + NC + l - 2] exist
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    cov[p] = 0.0;
+    xw[p] = (c0 + p < lim) ? xJ[c0 + p] : 0.0;
+  }
+#pragma unroll 4
+  for (int t = 0; t < l; ++t) {
+    const double xt = xs[t];
+#pragma unroll
+    for (int p = 0; p < P; ++p) cov[p] = fma(xt, xw[p], cov[p]);
+#pragma unroll
+    for (int p = 0; p < P - 1; ++p) xw[p] = xw[p + 1];
+    xw[P - 1] = (c0 + P + t < lim) ? xJ[c0 + P + t] : 0.0;
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p) cov[p] = (c0 + p < NC) ? fma(-muJ[c0 + p], sx, cov[p]) : 0.0;
+}
+
 template <int P, int NT, int CHM, class V>
 __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 : P <= 5 && NT <= 256 ? 2 : 1))
     k_mpdist(const MPArgs a) {
@@ -652,20 +680,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
     __syncthreads();
   }
   double cov[P];
-  {
-    const double sx = red[0];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int cl = tid * P + p;
-      double acc = 0.0;
-      if (cl < NC) {
-        const double* xc = xJ + cl;
-        for (int t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
-        acc = fma(-muJ[cl], sx, acc);
-      }
-      cov[p] = acc;
-    }
-  }
+  row0_dots<P>(cov, xs, xJ, muJ, red[0], tid * P, NC, l);
   __syncthreads();
   // ---- left edge (column J0) for rows 1..w-1: fresh dots against the centered column window
   {
@@ -883,20 +898,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
     __syncthreads();
   }
   double cov[P];
-  {
-    const double sx = red[0];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int cl = tid * P + p;
-      double acc = 0.0;
-      if (cl < NC) {
-        const double* xc = xJ + cl;
-        for (int t = 0; t < l; ++t) acc = fma(xs[t], xc[t], acc);
-        acc = fma(-muJ[cl], sx, acc);
-      }
-      cov[p] = acc;
-    }
-  }
+  row0_dots<P>(cov, xs, xJ, muJ, red[0], tid * P, NC, l);
   __syncthreads();
   {  // left edge (column J0) for rows 1..w-1
     const double mc = muJ[0];

@@ -575,6 +575,58 @@ __global__ void k_near_keys(const int* __restrict__ Dk, int64_t S, int64_t N, in
   }
 }
 
+// k_near_keys over chunks of segment rows [base, base+rows) arriving in order
+// (streamed key path): running smallest key, first segment, multiplicity,
+// next key and max key per window; finalize with k_near_finalize.
+__global__ void k_near_keys_acc(const int* __restrict__ Dk, int64_t rows, int64_t N, int64_t ld, int64_t base,
+                                int first, int* K1w, int32_t* s1w, int* n1w, int* K2w, int* kmaxw) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    int K1 = INT_MAX, K2 = INT_MAX, KM = INT_MIN, n1 = 0;
+    int64_t s1 = 0;
+    if (!first) {
+      K1 = K1w[j];
+      K2 = K2w[j];
+      KM = kmaxw[j];
+      n1 = n1w[j];
+      s1 = s1w[j];
+    }
+    for (int64_t r = 0; r < rows; ++r) {
+      const int K = Dk[r * ld + j];
+      KM = max(KM, K);
+      if (K < K1) {
+        K2 = K1;
+        K1 = K;
+        s1 = base + r;
+        n1 = 1;
+      } else if (K == K1) {
+        ++n1;
+      } else {
+        K2 = min(K2, K);
+      }
+    }
+    K1w[j] = K1;
+    K2w[j] = K2;
+    kmaxw[j] = KM;
+    n1w[j] = n1;
+    s1w[j] = (int32_t)s1;
+  }
+}
+__global__ void k_near_finalize(int64_t N, double twol, const int* __restrict__ K1w, const int32_t* __restrict__ s1w,
+                                const int* __restrict__ n1w, const int* __restrict__ K2w, int32_t* nearest,
+                                uint8_t* unc) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = n1w[j] == 1;
+    if (ok && K2w[j] != INT_MAX) {
+      double l1, h1, l2, h2;
+      kb_exact(K1w[j], twol, l1, h1);
+      kb_exact(K2w[j], twol, l2, h2);
+      ok = l2 > h1;
+    }
+    nearest[j] = s1w[j];
+    unc[j] = ok ? 0 : 1;
+  }
+}
+
 // windows with a flag set -> compact list (unordered)
 __global__ void k_flag_list(const uint8_t* __restrict__ flag, int64_t N, int cap, int64_t* list, int* cnt) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x)
@@ -598,9 +650,9 @@ __global__ void k_max_int(const int* __restrict__ v, int64_t N, int* out) {
 // Candidate (segment, window) pairs of listed windows, one warp per window:
 // mode 0 (attribution): segments whose lower bound lo(K) <= hi(K1w[j]);
 // mode 1 (profile_max): segments with K >= thr.
-__global__ void k_pairs(const int* __restrict__ Dk, int64_t S, int64_t ld, const int64_t* __restrict__ wins,
-                        int nwin, const int* __restrict__ K1w, int thr, int mode, double twol, int K15, int cap,
-                        int64_t* pseg, int64_t* pwin, int* cnt) {
+__global__ void k_pairs(const int* __restrict__ Dk, int64_t S, int64_t ld, int64_t base,
+                        const int64_t* __restrict__ wins, int nwin, const int* __restrict__ K1w, int thr, int mode,
+                        double twol, int K15, int cap, int64_t* pseg, int64_t* pwin, int* cnt) {
   const int lane = threadIdx.x & 31;
   const int wv = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (wv >= nwin) return;
@@ -632,7 +684,7 @@ __global__ void k_pairs(const int* __restrict__ Dk, int64_t S, int64_t ld, const
     if (mode == 0 ? K <= kthr : K >= kthr) {
       const int i = atomicAdd(cnt, 1);
       if (i < cap) {
-        pseg[i] = s;
+        pseg[i] = base + s;
         pwin[i] = j;
       }
     }
@@ -1050,6 +1102,30 @@ static bool use_keys(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
   return have > reserve && (size_t)S * N * sizeof(int) <= have - reserve;
 }
 
+static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N,
+                                    int64_t n, int64_t K, int64_t chunk, pst_snippets* res);
+
+// Streamed key path: the key matrix does not fit (or PASTILA_STREAM_KEYS forces it).
+static bool use_keys_streamed(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
+  if (const char* e = getenv("PASTILA_EXACT"))
+    if (atoi(e) > 0) return false;
+  if (getenv("PASTILA_STREAM_ROWS")) return false;
+  if (getenv("PASTILA_STREAM_KEYS")) return true;
+  return !use_keys(c, S, N, w);
+}
+// segments of keys per chunk: the free memory after the scratch reserve, at most S
+static int64_t key_chunk_rows(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 1;
+  const size_t have = fr + c->Dk_bytes + c->D_bytes;
+  const size_t seg_scratch = (size_t)N * 4 * (size_t)(w + w / 10 + 2);
+  const size_t reserve = std::max((size_t)12 << 30, 2 * seg_scratch) + (size_t)N * 8 * (24 + 16 + 8) +
+                         ((size_t)4 << 30);
+  if (have <= reserve) return 1;
+  const int64_t rows = (int64_t)((have - reserve) / ((size_t)N * sizeof(int)));
+  return rows >= S ? S : (rows < 1 ? 1 : rows);
+}
+
 int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, pst_snippets* res) {
   if (!valid(c)) return PST_EINVAL;
   PST_CUDA(cudaSetDevice(c->dev));
@@ -1064,7 +1140,18 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
     pst_set_error("snippet count %lld out of range [1, %lld]", (long long)K, (long long)S);
     return PST_EINVAL;
   }
-  if (use_keys(c, S, N, m - l + 1)) {
+  if (use_keys_streamed(c, S, N, m - l + 1)) {  // key matrix does not fit: streamed key path
+    if (c->D) {  // the exact matrix is not needed on this path
+      cudaFree(c->D);
+      c->D = nullptr;
+      c->D_bytes = 0;
+    }
+    const char* sk = getenv("PASTILA_STREAM_KEYS");
+    const int64_t chunk = sk ? std::max<int64_t>(1, atoll(sk)) : key_chunk_rows(c, S, N, m - l + 1);
+    const int r = run_select_keys_streamed(c, m, l, k, S, N, n, K, chunk, res);
+    if (r != 1) return r;
+    c->cert_stats[6]++;  // a certification cap was exceeded: recompute this length exactly
+  } else if (use_keys(c, S, N, m - l + 1)) {
     if (c->D) {  // the exact matrix is not needed on this path
       cudaFree(c->D);
       c->D = nullptr;
@@ -1354,9 +1441,10 @@ constexpr int CAP_W = 1 << 16;   // uncertain attribution / max windows
 constexpr int CAP_P = 1 << 18;   // exact (segment, window) evaluations
 
 struct CertBufs {
-  double *alo, *ahi, *crow, *carea, *pval;
-  int64_t *glist, *wins, *pseg, *pwin;
-  int *cnt, *kmaxw, *K1w;
+  double *alo, *ahi, *crow, *carea, *pval, *pval2;
+  int64_t *glist, *wins, *pseg, *pwin, *mwins, *pseg2, *pwin2;
+  int *cnt, *kmaxw, *K1w, *n1w, *K2w;
+  int32_t* s1w;
   uint8_t* unc;
 };
 static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
@@ -1369,7 +1457,9 @@ static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
   const size_t o_alo = take(S * 8), o_ahi = take(S * 8), o_crow = take((size_t)CAP_G * N * 8),
                o_carea = take(CAP_G * 8), o_pval = take((size_t)CAP_P * 8), o_gl = take(CAP_G * 8),
                o_w = take((size_t)CAP_W * 8), o_ps = take((size_t)CAP_P * 8), o_pw = take((size_t)CAP_P * 8),
-               o_cnt = take(4 * 4), o_km = take(N * 4), o_k1 = take(N * 4), o_unc = take(N);
+               o_cnt = take(4 * 4), o_km = take(N * 4), o_k1 = take(N * 4), o_unc = take(N),
+               o_mw = take((size_t)CAP_W * 8), o_ps2 = take((size_t)CAP_P * 8), o_pw2 = take((size_t)CAP_P * 8),
+               o_pv2 = take((size_t)CAP_P * 8), o_s1 = take(N * 4), o_n1 = take(N * 4), o_k2 = take(N * 4);
   PST_TRY(pst_ensure(&c->cert, &c->cert_bytes, off));
   char* p = (char*)c->cert;
   b.alo = (double*)(p + o_alo);
@@ -1385,22 +1475,63 @@ static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
   b.kmaxw = (int*)(p + o_km);
   b.K1w = (int*)(p + o_k1);
   b.unc = (uint8_t*)(p + o_unc);
+  b.mwins = (int64_t*)(p + o_mw);
+  b.pseg2 = (int64_t*)(p + o_ps2);
+  b.pwin2 = (int64_t*)(p + o_pw2);
+  b.pval2 = (double*)(p + o_pv2);
+  b.s1w = (int32_t*)(p + o_s1);
+  b.n1w = (int*)(p + o_n1);
+  b.K2w = (int*)(p + o_k2);
   return PST_OK;
 }
 
 // exact values of the listed (segment, window) pairs -> host vectors
-static int eval_pairs(pst_ctx* c, int64_t m, int64_t l, int64_t k, CertBufs& cb, int cnt, std::vector<int64_t>& seg,
-                      std::vector<int64_t>& win, std::vector<double>& val) {
+static int eval_pairs_at(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* dseg, const int64_t* dwin,
+                         double* dval, int cnt, std::vector<int64_t>& seg, std::vector<int64_t>& win,
+                         std::vector<double>& val) {
   seg.resize(cnt);
   win.resize(cnt);
   val.resize(cnt);
   if (cnt == 0) return PST_OK;
-  PST_TRY(launch_window_exact(c, m, l, k, cb.pseg, cb.pwin, cnt, cb.pval));
-  PST_CUDA(cudaMemcpyAsync(seg.data(), cb.pseg, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
-  PST_CUDA(cudaMemcpyAsync(win.data(), cb.pwin, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
-  PST_CUDA(cudaMemcpyAsync(val.data(), cb.pval, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_TRY(launch_window_exact(c, m, l, k, dseg, dwin, cnt, dval));
+  PST_CUDA(cudaMemcpyAsync(seg.data(), dseg, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(win.data(), dwin, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaMemcpyAsync(val.data(), dval, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
   c->cert_stats[4] += cnt;
+  return PST_OK;
+}
+static int eval_pairs(pst_ctx* c, int64_t m, int64_t l, int64_t k, CertBufs& cb, int cnt, std::vector<int64_t>& seg,
+                      std::vector<int64_t>& win, std::vector<double>& val) {
+  return eval_pairs_at(c, m, l, k, cb.pseg, cb.pwin, cb.pval, cnt, seg, win, val);
+}
+
+// exact nearest-segment fixes from evaluated (segment, window, value) triples:
+// per window the first argmin (value, then lowest segment)
+static int apply_nearest_fixes(pst_ctx* c, CertBufs& cb, const std::vector<int64_t>& ps,
+                               const std::vector<int64_t>& pw, const std::vector<double>& pv, int32_t* nearest) {
+  const size_t np = ps.size();
+  std::vector<size_t> ord(np);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](size_t a, size_t bb) {
+    if (pw[a] != pw[bb]) return pw[a] < pw[bb];
+    if (pv[a] != pv[bb]) return pv[a] < pv[bb];
+    return ps[a] < ps[bb];
+  });
+  std::vector<int64_t> fw, fs;
+  for (size_t i = 0; i < np; ++i)
+    if (i == 0 || pw[ord[i]] != pw[ord[i - 1]]) {
+      fw.push_back(pw[ord[i]]);
+      fs.push_back(ps[ord[i]]);
+    }
+  const int nf = (int)fw.size();
+  if (nf > 0) {
+    PST_CUDA(cudaMemcpyAsync(cb.wins, fw.data(), (size_t)nf * 8, cudaMemcpyHostToDevice, c->st));
+    PST_CUDA(cudaMemcpyAsync(cb.pseg, fs.data(), (size_t)nf * 8, cudaMemcpyHostToDevice, c->st));
+    k_set_nearest<<<(nf + 255) / 256, 256, 0, c->st>>>(cb.wins, cb.pseg, nf, nearest);
+    c->launches++;
+    PST_CUDA(cudaStreamSynchronize(c->st));  // fw / fs are host vectors
+  }
   return PST_OK;
 }
 
@@ -1486,7 +1617,7 @@ static int run_select_keys(pst_ctx* c, const int* Dk, int64_t m, int64_t l, int6
   std::vector<int64_t> ps, pw;
   std::vector<double> pv;
   if (nw > 0) {
-    k_pairs<<<(unsigned)((nw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, cb.wins, nw, cb.K1w, 0, 0, twol, K15, CAP_P,
+    k_pairs<<<(unsigned)((nw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, 0, cb.wins, nw, cb.K1w, 0, 0, twol, K15, CAP_P,
                                                                 cb.pseg, cb.pwin, cb.cnt + 1);
     c->launches++;
     int np = 0;
@@ -1545,8 +1676,8 @@ static int run_select_keys(pst_ctx* c, const int* Dk, int64_t m, int64_t l, int6
       int nmw = 0;
       PST_TRY(read_cnt(c, cb.cnt, nmw));
       if (nmw > CAP_W || nmw < 1) return 1;
-      k_pairs<<<(unsigned)((nmw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, cb.wins, nmw, cb.K1w, thr, 1, twol,
-                                                                   K15, CAP_P, cb.pseg, cb.pwin, cb.cnt + 1);
+      k_pairs<<<(unsigned)((nmw * 32 + 255) / 256), 256, 0, c->st>>>(Dk, S, N, 0, cb.wins, nmw, cb.K1w, thr, 1,
+                                                                   twol, K15, CAP_P, cb.pseg, cb.pwin, cb.cnt + 1);
       c->launches++;
       int np = 0;
       PST_TRY(read_cnt(c, cb.cnt + 1, np));
@@ -1561,6 +1692,182 @@ static int run_select_keys(pst_ctx* c, const int* Dk, int64_t m, int64_t l, int6
     memcpy(&bits, &pmax, 8);
     PST_CUDA(cudaMemcpyAsync(b.dmax, &bits, 8, cudaMemcpyHostToDevice, c->st));
     PST_CUDA(cudaStreamSynchronize(c->st));  // &bits is a stack variable
+  }
+  std::vector<int64_t> steps(K);
+  std::iota(steps.begin(), steps.end(), 0);
+  return finish_select(c, b, S, N, n, K, b.rows, steps, res);
+}
+
+// ---- streamed key path (S x N keys do not fit: C4, n = 1e7) -------------------
+// One certified greedy step from the area bounds of all S rows (alo/ahi filled).
+static int greedy_step_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, SelBufs& b,
+                            CertBufs& cb, int64_t step, std::vector<int64_t>& chosen) {
+  const double* cur = step == 0 ? nullptr : b.curve;
+  PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 4, c->st));
+  k_greedy_cands<<<1, 1024, 0, c->st>>>(cb.alo, cb.ahi, b.taken, S, CAP_G, cb.glist, cb.cnt);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  int nc = 0;
+  PST_TRY(read_cnt(c, cb.cnt, nc));
+  if (nc > CAP_G || nc < 1) return 1;
+  std::vector<int64_t> cand(nc);
+  PST_CUDA(cudaMemcpyAsync(cand.data(), cb.glist, (size_t)nc * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  std::sort(cand.begin(), cand.end());
+  c->cert_stats[1] += nc;
+  if (nc > 1) c->cert_stats[2]++;
+  for (int i = 0; i < nc; ++i) {
+    double* row = cb.crow + (size_t)i * N;
+    PST_TRY(launch_mpdist(c, m, l, k, cand[i], cand[i] + 1, row, N));
+    k_areas<<<1, 256, 0, c->st>>>(row, N, N, cur, cb.carea + i);
+    c->launches++;
+  }
+  std::vector<double> ca(nc);
+  PST_CUDA(cudaMemcpyAsync(ca.data(), cb.carea, (size_t)nc * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  int bi = 0;
+  for (int i = 1; i < nc; ++i)
+    if (ca[i] < ca[bi]) bi = i;
+  chosen[step] = cand[bi];
+  double* keep = b.rows + step * N;
+  PST_CUDA(cudaMemcpyAsync(keep, cb.crow + (size_t)bi * N, (size_t)N * 8, cudaMemcpyDeviceToDevice, c->st));
+  k_mark_taken<<<1, 1, 0, c->st>>>(b.taken, cand[bi]);
+  k_curve_row<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, keep, N);
+  c->launches += 2;
+  return PST_OK;
+}
+
+// Profiles are recomputed chunk by chunk (chunk segments of keys at a time) in
+// max(K, 2) passes: pass t feeds greedy step t's area bounds; pass 0 also
+// accumulates the per-window attribution state and maxima; pass 1 collects the
+// candidate (segment, window) pairs of the windows pass 0 left uncertain and
+// of profile_max.  Certification and exact resolution as run_select_keys.
+static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t n,
+                                    int64_t K, int64_t chunk, pst_snippets* res) {
+  const double twol = 2.0 * (double)l;
+  const float twolf = (float)twol;
+  int K15;
+  {
+    const double t = 1e-15;
+    unsigned long long bits;
+    memcpy(&bits, &t, 8);
+    K15 = (int)(bits >> 32);
+  }
+  const double dclip = e2d_h(2.0, twol);
+  SelBufs b;
+  PST_TRY(sel_bufs(c, S, N, n, K, true, b));
+  CertBufs cb;
+  PST_TRY(cert_bufs(c, S, N, cb));
+  PST_TRY(pst_ensure((void**)&c->Dk, &c->Dk_bytes, (size_t)chunk * N * sizeof(int)));
+  c->cert_stats[0]++;
+  c->cert_stats[7] += N;
+  PST_CUDA(cudaMemsetAsync(b.taken, 0, S, c->st));
+  k_fill<<<grid_for(N, 256), 256, 0, c->st>>>(b.curve, HUGE_VAL, N);
+  c->launches++;
+  std::vector<int64_t> chosen(K);
+  int nw = 0, nmw = 0, thr = 0;
+  double pmax = 0.0;
+  bool need_max = false;
+  const int64_t passes = std::max<int64_t>(K, 2);
+  for (int64_t pass = 0; pass < passes; ++pass) {
+    const bool greedy = pass < K;
+    const double* cur = pass == 0 ? nullptr : b.curve;
+    if (pass == 1) PST_CUDA(cudaMemsetAsync(cb.cnt + 1, 0, 12, c->st));  // pair counters [1] and [3]
+    for (int64_t s0 = 0; s0 < S; s0 += chunk) {
+      const int64_t rows = std::min(chunk, S - s0);
+      PST_TRY(launch_mpdist_keys(c, m, l, k, s0, s0 + rows, c->Dk, N));
+      if (greedy) {
+        k_areas_kb<<<(unsigned)rows, 256, 0, c->st>>>(c->Dk, N, N, cur, b.taken + s0, twolf, K15, dclip,
+                                                       cb.alo + s0, cb.ahi + s0);
+        c->launches++;
+      }
+      if (pass == 0) {
+        k_near_keys_acc<<<grid_for(N, 256), 256, 0, c->st>>>(c->Dk, rows, N, N, s0, s0 == 0 ? 1 : 0, cb.K1w,
+                                                            cb.s1w, cb.n1w, cb.K2w, cb.kmaxw);
+        c->launches++;
+      }
+      if (pass == 1) {
+        if (nw > 0) {
+          k_pairs<<<(unsigned)((nw * 32 + 255) / 256), 256, 0, c->st>>>(c->Dk, rows, N, s0, cb.wins, nw, cb.K1w, 0,
+                                                                      0, twol, K15, CAP_P, cb.pseg, cb.pwin,
+                                                                      cb.cnt + 1);
+          c->launches++;
+        }
+        if (need_max) {
+          k_pairs<<<(unsigned)((nmw * 32 + 255) / 256), 256, 0, c->st>>>(c->Dk, rows, N, s0, cb.mwins, nmw,
+                                                                       cb.K1w, thr, 1, twol, K15, CAP_P,
+                                                                       cb.pseg2, cb.pwin2, cb.cnt + 3);
+          c->launches++;
+        }
+      }
+      PST_CUDA(cudaGetLastError());
+    }
+    if (greedy) {
+      const int r = greedy_step_keys(c, m, l, k, S, N, b, cb, pass, chosen);
+      if (r != PST_OK) return r;
+    }
+    if (pass == 0) {  // attribution state complete: certified windows and the lists for pass 1
+      k_near_finalize<<<grid_for(N, 256), 256, 0, c->st>>>(N, twol, cb.K1w, cb.s1w, cb.n1w, cb.K2w, b.nearest,
+                                                          cb.unc);
+      PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 4, c->st));
+      k_flag_list<<<grid_for(N, 256), 256, 0, c->st>>>(cb.unc, N, CAP_W, cb.wins, cb.cnt);
+      c->launches += 2;
+      PST_TRY(read_cnt(c, cb.cnt, nw));
+      if (nw > CAP_W) return 1;
+      c->cert_stats[3] += nw;
+      static const int kIntMin = INT_MIN;
+      PST_CUDA(cudaMemcpyAsync(cb.cnt + 2, &kIntMin, 4, cudaMemcpyHostToDevice, c->st));
+      k_max_int<<<grid_for(N, 256, 1024), 256, 0, c->st>>>(cb.kmaxw, N, cb.cnt + 2);
+      c->launches++;
+      int kmax = 0;
+      PST_TRY(read_cnt(c, cb.cnt + 2, kmax));
+      double lo, hi;
+      kb_exact_h(kmax, twol, lo, hi);
+      if (lo == hi) {
+        pmax = lo;
+      } else {
+        need_max = true;
+        thr = kmax;
+        int guard = 0;
+        while (thr > K15) {
+          double l2, h2;
+          kb_exact_h(thr - 1, twol, l2, h2);
+          if (h2 < lo) break;
+          --thr;
+          if (++guard > 1024) return 1;
+        }
+        k_kmax_flag<<<grid_for(N, 256), 256, 0, c->st>>>(cb.kmaxw, N, thr, cb.unc);
+        PST_CUDA(cudaMemsetAsync(cb.cnt, 0, 4, c->st));
+        k_flag_list<<<grid_for(N, 256), 256, 0, c->st>>>(cb.unc, N, CAP_W, cb.mwins, cb.cnt);
+        c->launches += 2;
+        PST_TRY(read_cnt(c, cb.cnt, nmw));
+        if (nmw > CAP_W || nmw < 1) return 1;
+      }
+    }
+  }
+  PST_CUDA(cudaMemcpyAsync(b.best, chosen.data(), K * 8, cudaMemcpyHostToDevice, c->st));
+  std::vector<int64_t> ps, pw;
+  std::vector<double> pv;
+  if (nw > 0) {
+    int np = 0;
+    PST_TRY(read_cnt(c, cb.cnt + 1, np));
+    if (np > CAP_P) return 1;
+    PST_TRY(eval_pairs(c, m, l, k, cb, np, ps, pw, pv));
+    PST_TRY(apply_nearest_fixes(c, cb, ps, pw, pv, b.nearest));
+  }
+  if (need_max) {
+    int np = 0;
+    PST_TRY(read_cnt(c, cb.cnt + 3, np));
+    if (np > CAP_P || np < 1) return 1;
+    PST_TRY(eval_pairs_at(c, m, l, k, cb.pseg2, cb.pwin2, cb.pval2, np, ps, pw, pv));
+    c->cert_stats[5] += np;
+    for (double v : pv) pmax = std::max(pmax, v);
+  }
+  {
+    unsigned long long bits;
+    memcpy(&bits, &pmax, 8);
+    PST_CUDA(cudaMemcpyAsync(b.dmax, &bits, 8, cudaMemcpyHostToDevice, c->st));
+    PST_CUDA(cudaStreamSynchronize(c->st));
   }
   std::vector<int64_t> steps(K);
   std::iota(steps.begin(), steps.end(), 0);

@@ -183,3 +183,26 @@ def test_select_length_key_path_equals_exact_path():
     assert [c.score for c in ra.candidates] == [c.score for c in rb.candidates]
     for m in grid:
         _same(resa[m], resb[m])
+
+
+@pytest.mark.parametrize("chunk", ["1", "7", "64"])
+@pytest.mark.parametrize("case", ["planted", "two_regime_exact"])
+def test_streamed_key_path_equals_exact_path(monkeypatch, case, chunk):
+    """Key matrix streamed in chunks of segments (C4 mode: max(K, 2) profile passes,
+    attribution state accumulated across chunks, candidate pairs collected in pass 1)
+    == the exact path, field by field."""
+    n = 20_000
+    if case == "planted":
+        x, _ = planted_walk(n, m_act=120, A=3, seed=8)
+    else:
+        x, _ = two_regime_series(n, period=32, block_len=64, noise=0.0)
+    s = P.TimeSeries(x)
+    b = _run(s, 96, 3, exact=True)
+    monkeypatch.setenv("PASTILA_STREAM_KEYS", chunk)
+    _stats(reset=True)
+    a = _run(s, 96, 3, exact=False)
+    st = _stats()
+    _same(a, b)
+    assert st[0] == 1
+    if case == "planted":
+        assert st[6] == 0

@@ -1440,11 +1440,8 @@ struct OutT<int> {
 // (answers may be tiny negative residues, so no sentinel value is used).
 // Also returns #(B < ans) and #(B <= ans) for the lane's incremental B counts.
 template <int TM, class V>
-__device__ __forceinline__ V solve_window(const V* __restrict__ ab, const V* BA, int w, int k, int R, int Tp, int L,
-                                          int r, int lane, bool fresh, V piv, int lt0, int le0, int& ltB, int& leB,
-                                          V* colbuf) {
-  const V* Ac = ab + r * 32 + L;
-  const V* Bc = BA + L * R + r;
+__device__ __forceinline__ V solve_col(const V* __restrict__ Ac, const V* Bc, int Tp, int w, int k, int lane,
+                                       bool fresh, V piv, int lt0, int le0, int& ltB, int& leB, V* colbuf) {
   V x;
   int b1 = 0, b2 = 0;
   if constexpr (TM > 0) {
@@ -1480,6 +1477,12 @@ __device__ __forceinline__ V solve_window(const V* __restrict__ ab, const V* BA,
   ltB = __reduce_add_sync(FULLMASK, b1);
   leB = __reduce_add_sync(FULLMASK, b2);
   return x;
+}
+template <int TM, class V>
+__device__ __forceinline__ V solve_window(const V* __restrict__ ab, const V* BA, int w, int k, int R, int Tp, int L,
+                                          int r, int lane, bool fresh, V piv, int lt0, int le0, int& ltB, int& leB,
+                                          V* colbuf) {
+  return solve_col<TM, V>(ab + r * 32 + L, BA + L * R + r, Tp, w, k, lane, fresh, piv, lt0, le0, ltB, leB, colbuf);
 }
 
 // Lane pass of one window: counts of the pivot p and the two nearest values
@@ -1788,6 +1791,150 @@ __global__ void __launch_bounds__(WX_NT) k_window_exact(const WinArgs a) {
   }
 }
 
+// Grouped lane-run selection (lane pass): one CTA per (G consecutive tiles,
+// segment), so each lane's run of consecutive windows spans G tiles -- G times
+// fewer cold run starts (each is a warp-cooperative solve from scratch) than
+// one run per tile.  Window jg of the group lives in tile g = jg / T at
+// tile-local jl; its row minima are in that tile's lane-run scratch, its
+// column-minima window in that tile's BA (all G BA arrays in shared memory).
+template <int NWS, int TM, class V>
+__global__ void __launch_bounds__(NWS * 32, 1) k_select_grp(const MPArgs a, int NCmax, int G, int ntile) {
+  using O = typename OutT<V>::type;
+  extern __shared__ __align__(16) unsigned char smsel[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = (int)a.w, R = (int)a.R, Tp = (int)a.Tp, k = (int)a.k, T = (int)a.T;
+  const int t0 = blockIdx.x * G;
+  const int ntl = min(G, ntile - t0);
+  const int64_t J0g = (int64_t)t0 * T;
+  const int NJg = (int)min((int64_t)ntl * T, a.N - J0g);
+  V* BAs = (V*)smsel;                        // [G][NCmax]
+  V* colbuf = BAs + G * NCmax + warp * w;    // [w] per warp, long windows (TM == 0) only
+  const int64_t cta0 = (int64_t)blockIdx.y * ntile + t0;
+  for (int g = 0; g < ntl; ++g) {
+    const int NJt = (int)min((int64_t)T, a.N - (J0g + (int64_t)g * T));
+    const int NCt = NJt + w - 1;
+    const V* bag = (const V*)a.ba + (cta0 + g) * NCmax;
+    for (int c = tid; c < NCt; c += NWS * 32) BAs[g * NCmax + c] = bag[c];
+  }
+  __syncthreads();
+  const double twol = 2.0 * (double)a.l;
+  O* Drow = (O*)a.D + (a.rowD0 + blockIdx.y) * a.ldD + J0g;
+  const int Rg = (NJg + 31) / 32;
+  const int rper = (Rg + NWS - 1) / NWS;
+  const int r0 = warp * rper, r1 = min(Rg, r0 + rper);
+  if (r0 >= r1) return;
+  const V* abase = (const V*)a.ab + cta0 * ((int64_t)w * Tp);
+  const int64_t tstride = (int64_t)w * Tp;
+  // column pointers of group window jg: AB column base and BA window base
+  auto col = [&](int jg, const V*& Ac, const V*& Bc) {
+    const int g = jg / T, jl = jg - g * T;
+    Ac = abase + g * tstride + (jl % R) * 32 + jl / R;
+    Bc = BAs + g * NCmax + jl;
+  };
+  const int jl0 = lane * Rg;  // first window of this lane's run
+  if (2 * w <= k) {           // the k-th smallest is the maximum (mpdist.py:229-230)
+    for (int r = r0; r < r1; ++r) {
+      const int jg = jl0 + r;
+      if (jg >= NJg) continue;
+      const V *Ac, *Bc;
+      col(jg, Ac, Bc);
+      V mx = VT<V>::ninf();
+      for (int i = 0; i < w; ++i) mx = vmax(mx, vmax(__ldg(Ac + (int64_t)i * Tp), Bc[i]));
+      put_out(Drow, jg, mx, twol);
+    }
+    return;
+  }
+  // run starts, lanes in turn, each seeded with the previous lane's answer
+  V p = VT<V>::of(0.0);
+  {
+    V prev = VT<V>::of(0.0);
+    for (int L = 0; L < 32; ++L) {
+      const int jg = L * Rg + r0;
+      if (jg >= NJg) break;  // warp-uniform
+      const V *Ac, *Bc;
+      col(jg, Ac, Bc);
+      int b1, b2;
+      prev = solve_col<TM, V>(Ac, Bc, Tp, w, k, lane, L == 0, prev, -1, -1, b1, b2, colbuf);
+      if (lane == L) p = prev;
+    }
+    if (jl0 + r0 < NJg) put_out(Drow, jl0 + r0, p, twol);
+  }
+  for (int r = r0 + 1; r < r1; ++r) {
+    const int jg = jl0 + r;
+    const bool ok = jg < NJg;
+    const V *Ap, *Bp;
+    col(ok ? jg : jl0 + r0, Ap, Bp);
+    int lt = 0, le = 0;
+    V b1 = VT<V>::ninf(), b2 = VT<V>::ninf(), a1 = VT<V>::inf(), a2 = VT<V>::inf();
+    constexpr int kUn = TM >= 7 || TM == 0 ? 16 : 8;
+#pragma unroll kUn
+    for (int i = 0; i < w; ++i) {
+      lane_acc<V>(__ldg(Ap + (int64_t)i * Tp), p, lt, le, b1, b2, a1, a2);
+      lane_acc<V>(Bp[i], p, lt, le, b1, b2, a1, a2);
+    }
+    V ans = p;
+    bool done = lt < k && k <= le;
+    if (!done) {
+      if (k <= lt) {
+        const int need = lt - k + 1;
+        if (need == 1) { ans = b1; done = true; }
+        else if (need == 2) { ans = b2; done = true; }
+      } else {
+        const int need = k - le;
+        if (need == 1) { ans = a1; done = true; }
+        else if (need == 2) { ans = a2; done = true; }
+      }
+    }
+    unsigned pend = __ballot_sync(FULLMASK, ok && !done);
+    while (pend) {
+      const int L = __ffs(pend) - 1;
+      pend &= pend - 1;
+      const V pl = __shfl_sync(FULLMASK, p, L);
+      const int ltl = __shfl_sync(FULLMASK, lt, L), lel = __shfl_sync(FULLMASK, le, L);
+      const V *Ac, *Bc;
+      col(L * Rg + r, Ac, Bc);
+      int b1c, b2c;
+      const V x = solve_col<TM, V>(Ac, Bc, Tp, w, k, lane, false, pl, ltl, lel, b1c, b2c, colbuf);
+      if (lane == L) ans = x;
+    }
+    p = ans;
+    if (ok) put_out(Drow, jg, p, twol);
+  }
+}
+
+template <int NWS, int TM, class V>
+int launch_grp_w(pst_ctx* c, const MPArgs& a, int nseg, int ntile, int NCmax, int G) {
+  const size_t smem = (size_t)(G * NCmax + (TM == 0 ? NWS * a.w : 0)) * sizeof(V);
+  auto kern = k_select_grp<NWS, TM, V>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      pst_set_error("cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+      return PST_ECUDA;
+    }
+  }
+  dim3 grid((unsigned)((ntile + G - 1) / G), (unsigned)nseg);
+  kern<<<grid, NWS * 32, smem, c->st2>>>(a, NCmax, G, ntile);
+  c->launches++;
+  PST_CUDA(cudaGetLastError());
+  return PST_OK;
+}
+template <class V>
+int launch_grp(pst_ctx* c, const MPArgs& a, int nseg, int ntile, int NCmax, int G) {
+  switch ((int)((a.w + 31) >> 5)) {
+    case 1: return launch_grp_w<1, 1, V>(c, a, nseg, ntile, NCmax, G);
+    case 2: return launch_grp_w<1, 2, V>(c, a, nseg, ntile, NCmax, G);
+    case 3: return launch_grp_w<1, 3, V>(c, a, nseg, ntile, NCmax, G);
+    case 4: return launch_grp_w<1, 4, V>(c, a, nseg, ntile, NCmax, G);
+    case 5: return launch_grp_w<1, 5, V>(c, a, nseg, ntile, NCmax, G);
+    case 6: return launch_grp_w<1, 6, V>(c, a, nseg, ntile, NCmax, G);
+    case 7: return launch_grp_w<1, 7, V>(c, a, nseg, ntile, NCmax, G);
+    case 8: return launch_grp_w<1, 8, V>(c, a, nseg, ntile, NCmax, G);
+    case 9: return launch_grp_w<1, 9, V>(c, a, nseg, ntile, NCmax, G);
+    default: return launch_grp_w<1, 0, V>(c, a, nseg, ntile, NCmax, G);
+  }
+}
+
 template <int P, int NT, int CHM, class V>
 int launch_p(pst_ctx* c, const MPArgs& a, dim3 grid, size_t smem) {
   auto kern = k_mpdist<P, NT, CHM, V>;
@@ -2089,6 +2236,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const size_t ab_cta = (size_t)w * (size_t)Tp * SV;
   const size_t per_cta = ab_cta + (size_t)NCmax * SV;
   size_t budget = (size_t)6 << 30;
+  if (const char* e = getenv("PASTILA_SCRATCH_GB")) budget = (size_t)atoll(e) << 30;  // tuning experiments
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 3 + c->scratch_bytes);
@@ -2102,7 +2250,14 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   const size_t buf_bytes = per_cta * (size_t)ntile * (size_t)segs_per;
   PST_TRY(pst_ensure((void**)&c->scratch, &c->scratch_bytes, 2 * buf_bytes));
   if (!c->st2) {
-    PST_CUDA(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+    // selection stream priority (tuning experiments, PASTILA_SELPRIO: <0 = higher priority)
+    int prio = 0;
+    if (const char* e = getenv("PASTILA_SELPRIO")) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least (0), hi = greatest (negative)
+      prio = atoi(e) < 0 ? hi : lo;
+    }
+    PST_CUDA(cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, prio));
     for (int bi = 0; bi < 2; ++bi) {
       PST_CUDA(cudaEventCreateWithFlags(&c->ev_rows[bi], cudaEventDisableTiming));
       PST_CUDA(cudaEventCreateWithFlags(&c->ev_sel[bi], cudaEventDisableTiming));
@@ -2130,6 +2285,13 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   }
   const size_t smem = G.v2 ? smem_rowsP(l, w, 256, P, SV) : smem_row1(chm == 0, l, w, NCmax, SV);
   const size_t smem2 = smem_row2(l, w, NCmax, SV);
+  // grouped selection (one lane run over G tiles): opt-in experiment, PASTILA_GRP = G.  Measured
+  // 4-6x slower for G >= 2: the per-tile lane-run scratch layout is no longer coalesced for the
+  // group's run length (the row kernel would have to store in the group's layout).  0 = per-tile
+  // k_select_run (default).
+  int grp = 0;
+  if (const char* e = getenv("PASTILA_GRP")) grp = atoi(e);
+  if (grp > 0 && (size_t)grp * NCmax * SV + (size_t)w * SV > (c->smem_optin ? c->smem_optin : 232448)) grp = 1;
   // the selection stream starts after everything queued before on the main stream
   PST_CUDA(cudaEventRecord(c->ev_rows[1], c->st));
   PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[1], 0));
@@ -2160,7 +2322,10 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
     PST_CUDA(cudaEventRecord(c->ev_rows[bi], c->st));
     PST_CUDA(cudaStreamWaitEvent(c->st2, c->ev_rows[bi], 0));
     if (kt) PST_TRY(kev_begin(c, c->st2, ke, 1));
-    r = launch_sel<V>(c, a, grid, (int)NCmax);
+    if (grp > 0)
+      r = launch_grp<V>(c, a, (int)ns, (int)ntile, (int)NCmax, grp);
+    else
+      r = launch_sel<V>(c, a, grid, (int)NCmax);
     if (r != PST_OK) return r;
     if (kt) PST_TRY(kev_end(c, c->st2, ke));
     PST_CUDA(cudaEventRecord(c->ev_sel[bi], c->st2));

@@ -1097,7 +1097,8 @@ static bool use_keys(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
   const size_t have = fr + c->Dk_bytes + c->D_bytes;
-  const size_t seg_scratch = (size_t)N * 4 * (size_t)(w + w / 10 + 2);
+  // profile-kernel scratch of the exact single-segment profiles of greedy candidates (f64 AB tiles, two buffers)
+  const size_t seg_scratch = (size_t)N * 8 * (size_t)(w + w / 10 + 2);
   const size_t reserve = std::max((size_t)8 << 30, 2 * seg_scratch) + (size_t)N * 8 * (24 + 16) + ((size_t)3 << 30);
   return have > reserve && (size_t)S * N * sizeof(int) <= have - reserve;
 }
@@ -1118,7 +1119,8 @@ static int64_t key_chunk_rows(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 1;
   const size_t have = fr + c->Dk_bytes + c->D_bytes;
-  const size_t seg_scratch = (size_t)N * 4 * (size_t)(w + w / 10 + 2);
+  // profile-kernel scratch of the exact single-segment profiles of greedy candidates (f64 AB tiles, two buffers)
+  const size_t seg_scratch = (size_t)N * 8 * (size_t)(w + w / 10 + 2);
   const size_t reserve = std::max((size_t)12 << 30, 2 * seg_scratch) + (size_t)N * 8 * (24 + 16 + 8) +
                          ((size_t)4 << 30);
   if (have <= reserve) return 1;

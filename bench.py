@@ -33,6 +33,11 @@ import threading
 import time
 from pathlib import Path
 
+_T_START = time.perf_counter()
+# wall-time budget of the whole run (the driver kills the bench at 1800 s): the
+# e2e sweep and the CPU sample are skipped, and said so, when they would not fit
+BUDGET_S = float(os.environ.get("PASTILA_BENCH_BUDGET_S", "1740"))
+
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
@@ -340,14 +345,24 @@ def main():
             return {p.snippet_size: P.criterion_score(r) for p, r, _ in timings}
         rep, results = P.select_length(s, grid, K_SNIPPETS, training_log=False)
         return {c.snippet_size: c.score for c in rep.candidates}
+    def elapsed_all():  # wall time since start, max over ranks (a decision every rank takes alike)
+        el = time.perf_counter() - _T_START
+        if ws > 1 or args.force_dist:
+            t = torch.tensor([el], dtype=torch.float64, device=red_dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        return el
+
     barrier()
-    t0 = time.perf_counter()
-    e2e_res = e2e_step()
-    e2e_s = time.perf_counter() - t0
-    if ws > 1 or args.force_dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_res, e2e_s = None, None
+    if elapsed_all() + 1.2 * ms / 1e3 + 30.0 <= BUDGET_S:
+        t0 = time.perf_counter()
+        e2e_res = e2e_step()
+        e2e_s = time.perf_counter() - t0
+        if ws > 1 or args.force_dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
 
     total_pairs = sum(pairs_of(N_SERIES, m) for m in grid)
     if sharded:  # this rank's segment range of every length
@@ -364,8 +379,11 @@ def main():
     achieved = FP64_FLOPS_PER_PAIR * my_pairs * args.steps / (kms.value / 1e3) / 1e12 if kms.value > 0 else None
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        v, sample = cpu_sample_pairs_per_s(x)
-        cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample, "host": host_cpu()}
+        if time.perf_counter() - _T_START + 30.0 <= BUDGET_S:
+            v, sample = cpu_sample_pairs_per_s(x)
+            cpu = {"value": v, "unit": "pairs/s", "cores": 1, "kind": "port", "sample": sample, "host": host_cpu()}
+        else:
+            cpu = {"value": None, "unit": "pairs/s", "skipped": f"wall-time budget {BUDGET_S:.0f} s"}
     issue = None
     ip = next((ROOT / "profiles" / f for f in ("r02_full_m256_summary.json", "r01_full_g256_summary.json")
                if (ROOT / "profiles" / f).exists()), None)
@@ -390,8 +408,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "seconds_per_sweep": ms / 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(ws, args.shard), "host": host_cpu(),
-            "e2e": {"value": total_pairs / e2e_s, "unit": "pairs/s", "seconds": e2e_s,
-                    "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)},
+            "e2e": ({"value": total_pairs / e2e_s, "unit": "pairs/s", "seconds": e2e_s,
+                     "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)} if e2e_s else
+                    {"value": None, "unit": "pairs/s", "skipped": f"wall-time budget {BUDGET_S:.0f} s",
+                     "h2d_bytes_per_step": int(x.nbytes), "d2h_bytes_per_step": int(d2h)}),
             "roofline": {"bound": "fp64", "kernel": "profile pass (k_mpdist<int> row loop + k_select_run<int> "
                                                     "selection, key path)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -404,7 +424,7 @@ def main():
                 ["lengths", "greedy_exact_candidates", "greedy_steps_multi", "attribution_uncertain_windows",
                  "exact_window_evals", "max_candidates", "fallbacks_to_exact", "windows"], cert.tolist())},
                 "meaning": "key-path decisions resolved with exact fp64 values (pastila.cu run_select_keys)"},
-            "m_best": max(e2e_res.items(), key=lambda t: (t[1], -t[0]))[0],
+            "m_best": max(e2e_res.items(), key=lambda t: (t[1], -t[0]))[0] if e2e_res else None,
         }
         if args.grid:
             line["config"]["dev_grid_override"] = grid

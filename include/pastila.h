@@ -153,6 +153,13 @@ int pst_window_exact(pst_ctx* ctx, int64_t m, int64_t l, int64_t k, const int64_
  * candidate, uncertain attribution windows, exact window evaluations,
  * profile_max candidates, fallbacks to the exact path, windows].         */
 int pst_cert_stats(pst_ctx* ctx, int64_t* out8, int reset);
+/* Streamed key path (profile keys larger than HBM, e.g. C4): greedy passes
+ * after the second recompute only the segments whose area lower bound (from
+ * per-block key minima kept since pass 0) can still win (snippets.py:201-210
+ * decides the same argmin).  Counters since the last reset: [pruned passes,
+ * rows recomputed in them, pruned passes that fell back to a full pass,
+ * rows of those].                                                          */
+int pst_prune_stats(pst_ctx* ctx, int64_t* out4, int reset);
 /* ---- multi-GPU data plane (segment-row sharding; the
  * reference has none: its workers are processes, scheduler.py:373-405) ----
  * One NCCL communicator per context (NCCL is dlopen'ed).  Rank 0 creates the

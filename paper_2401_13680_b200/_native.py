@@ -61,6 +61,7 @@ SIGNATURES = {
     "pst_profile_keys": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _ip]),
     "pst_window_exact": (C.c_int, [_vp, _i64, _i64, _i64, _lp, _lp, _i64, _dp]),
     "pst_cert_stats": (C.c_int, [_vp, _lp, C.c_int]),
+    "pst_prune_stats": (C.c_int, [_vp, _lp, C.c_int]),
     "pst_kernel_times": (C.c_int, [_vp, _dp]),
     "pst_comm_init": (C.c_int, [_vp, C.c_char_p, C.c_int, C.c_int]),
     "pst_comm_destroy": (C.c_int, [_vp]),

@@ -84,6 +84,13 @@ struct pst_ctx {
   size_t work_bytes = 0;
   void* aux = nullptr;       // per-length preparation scratch (hash sort); never holds live results
   size_t aux_bytes = 0;
+  // streamed key path: per-block key minima of every profile row + greedy-pass
+  // lower-bound scratch (pruned greedy passes); freed after each length
+  void* prune = nullptr;
+  size_t prune_bytes = 0;
+  // [0] pruned greedy passes, [1] rows recomputed in them, [2] pruned passes
+  // that fell back to a full pass (too many candidates), [3] rows of those passes
+  int64_t prune_stats[4] = {0, 0, 0, 0};
   int64_t launches = 0;
   double* dbg = nullptr;
   size_t dbg_bytes = 0;
@@ -114,7 +121,8 @@ struct MPArgs {
   const unsigned long long* hash;  // window hashes (exact-repeat zeros, see same_window in mpdist.cu)
   int rep;                         // apply the exact-repeat rule (always, except the A/B test knob)
   int64_t n, l, m, w, k, Nl, N, T;
-  int64_t seg0;      // segment of blockIdx.y == 0
+  int64_t seg0;      // segment of blockIdx.y == 0 (segs: its position in the list)
+  const int64_t* segs;  // optional device list of segment indices (nullptr: seg0 + blockIdx.y)
   void* D;           // output rows (segment seg0+blockIdx.y -> row rowD0+blockIdx.y): double d / int key
   int64_t ldD, rowD0;
   void* ab;          // scratch, w*Tp values V per CTA, lane-run order (see mpdist.cu)
@@ -144,6 +152,8 @@ int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, i
 // P_ABBA element instead of the distance (exact d lies in [f(lo(key)), f(hi(key))]).
 int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
                        int* Dk_dev, int64_t ld);
+int launch_mpdist_keys_list(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* segs, int64_t cnt,
+                            int* Dk_dev, int64_t ld);
 // exact profile values at single (segment, window) pairs, bit-identical to the
 // full profile kernels: out[i] = D[seg[i]][win[i]] (device arrays, cnt entries).
 int kernel_times_read(pst_ctx* c, double* out2);

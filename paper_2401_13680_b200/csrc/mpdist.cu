@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128 ? 4 : P <= 3 && NT <= 256 ? 3 :
   constexpr int NW = NT / 32;
   constexpr int NCmax = NT * P;
   const int l = (int)a.l, w = (int)a.w, T = (int)a.T;
-  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t q0 = (a.segs ? a.segs[a.seg0 + blockIdx.y] : a.seg0 + blockIdx.y) * a.m;
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(NT, (P <= 5 && NT <= 256 ? 2 : 1)) k_mpdist2(c
   constexpr int NW = NT / 32;
   constexpr int NCmax = NT * P;
   const int l = (int)a.l, w = (int)a.w;
-  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t q0 = (a.segs ? a.segs[a.seg0 + blockIdx.y] : a.seg0 + blockIdx.y) * a.m;
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
@@ -1106,7 +1106,7 @@ __global__ void __launch_bounds__(NT, sizeof(V) == 4 ? 2 : 1) k_rowsP(const MPAr
   constexpr int NCmax = NT * P;
   const int l = (int)a.l, w = (int)a.w;
   const int D = (w - 1) / P, L2 = D - 1;
-  const int64_t q0 = (a.seg0 + blockIdx.y) * a.m;
+  const int64_t q0 = (a.segs ? a.segs[a.seg0 + blockIdx.y] : a.seg0 + blockIdx.y) * a.m;
   const int64_t J0 = (int64_t)blockIdx.x * a.T;
   const int NJ = (int)min(a.T, a.N - J0);
   const int NC = NJ + w - 1;
@@ -2167,19 +2167,19 @@ int tile_geom(pst_ctx* c, int64_t m, int64_t l, TileGeom& G) {
 // Profiles of segments [seg_lo, seg_hi) into D_dev rows 0.. (row stride ld).
 template <class V>
 static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
-                              void* D_dev, int64_t ld);
+                              void* D_dev, int64_t ld, const int64_t* segs);
 
 template <class V>
 static int launch_timed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, void* D_dev,
-                        int64_t ld) {
+                        int64_t ld, const int64_t* segs = nullptr) {
   PST_TRY(pst_ensure_len(c, l));
-  if (!c->timing) return launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  if (!c->timing) return launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld, segs);
   cudaEvent_t e0, e1;
   PST_CUDA(cudaEventCreate(&e0));
   PST_CUDA(cudaEventCreate(&e1));
   PST_CUDA(cudaEventRecord(e0, c->st));
   const int64_t before = c->launches;
-  int r = launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld);
+  int r = launch_mpdist_impl<V>(c, m, l, k, seg_lo, seg_hi, D_dev, ld, segs);
   PST_CUDA(cudaEventRecord(e1, c->st));
   if (!c->tev) c->tev = new std::vector<std::pair<cudaEvent_t, cudaEvent_t>>();
   ((std::vector<std::pair<cudaEvent_t, cudaEvent_t>>*)c->tev)->push_back({e0, e1});
@@ -2195,6 +2195,12 @@ int launch_mpdist(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, i
 int launch_mpdist_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi, int* Dk_dev,
                        int64_t ld) {
   return launch_timed<int>(c, m, l, k, seg_lo, seg_hi, Dk_dev, ld);
+}
+
+// Key rows of the listed segments (device list segs[0..cnt)) into rows 0..cnt-1.
+int launch_mpdist_keys_list(pst_ctx* c, int64_t m, int64_t l, int64_t k, const int64_t* segs, int64_t cnt,
+                            int* Dk_dev, int64_t ld) {
+  return launch_timed<int>(c, m, l, k, 0, cnt, Dk_dev, ld, segs);
 }
 
 struct KEv {
@@ -2221,8 +2227,10 @@ static int kev_end(pst_ctx* c, cudaStream_t st, KEv& e) {
 }
 
 template <class V>
+// segs != nullptr: [seg_lo, seg_hi) are positions in the device list segs of
+// segment indices (output row = position - seg_lo), not segment indices.
 static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t seg_lo, int64_t seg_hi,
-                              void* D_dev, int64_t ld) {
+                              void* D_dev, int64_t ld, const int64_t* segs) {
   const int64_t n = c->n, w = m - l + 1, Nl = n - l + 1, N = n - m + 1;
   const bool kt = ktime_on(c);
   KEv ke;
@@ -2273,6 +2281,7 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   a.n = n; a.l = l; a.m = m; a.w = w; a.k = k; a.Nl = Nl; a.N = N; a.T = T;
   a.R = R; a.Tp = Tp;
   a.D = D_dev; a.ldD = ld;
+  a.segs = segs;
   a.dbg_ba = nullptr;
   a.dbg_flags = getenv("PASTILA_DBGF") ? atoi(getenv("PASTILA_DBGF")) : 0;
   if (a.dbg_flags & 16) {  // move histogram: 8 counters, read with pst_debug_hist

@@ -488,12 +488,15 @@ __device__ __forceinline__ void kb_fast(int K, float twolf, int K15, double dcli
 // Greedy-step area bounds, same reduction structure as k_areas (per-thread
 // strided fp64 sums + block_sum), so that fp-monotonicity makes
 // alo[s] <= area*[s] <= ahi[s] hold for the rounded sums too.
+// segs != nullptr: row blockIdx.x holds segment segs[blockIdx.x] (taken/alo/ahi index)
 __global__ void __launch_bounds__(256) k_areas_kb(const int* __restrict__ Dk, int64_t N, int64_t ld,
                                                   const double* __restrict__ curve, const uint8_t* __restrict__ taken,
-                                                  float twolf, int K15, double dclip, double* alo, double* ahi) {
+                                                  float twolf, int K15, double dclip, double* alo, double* ahi,
+                                                  const int64_t* __restrict__ segs = nullptr) {
   __shared__ double sh[8];
-  if (taken[blockIdx.x]) {
-    if (threadIdx.x == 0) alo[blockIdx.x] = ahi[blockIdx.x] = PST_INF;
+  const int64_t s = segs ? segs[blockIdx.x] : blockIdx.x;
+  if (taken[s]) {
+    if (threadIdx.x == 0) alo[s] = ahi[s] = PST_INF;
     return;
   }
   const int* row = Dk + blockIdx.x * ld;
@@ -512,8 +515,90 @@ __global__ void __launch_bounds__(256) k_areas_kb(const int* __restrict__ Dk, in
   const double tl = block_sum<256>(al, sh);
   const double th = block_sum<256>(ah, sh);
   if (threadIdx.x == 0) {
-    alo[blockIdx.x] = tl;
-    ahi[blockIdx.x] = th;
+    alo[s] = tl;
+    ahi[s] = th;
+  }
+}
+
+// ---- pruned greedy passes of the streamed key path -------------------------
+// Pass 0 keeps, per profile row s and block b of B windows, the smallest key
+// Bm[s][b].  A later greedy pass (curve fixed) then has, for every segment,
+//   LB[s] = sum_b sum_{j in b} min(curve_j, lo(Bm[s][b])) <= area*[s]
+// (lo = kb_fast's lower bound, monotone in the key), and only the segments
+// with LB[s] <= (an exact upper bound of the winner's area) are recomputed.
+__global__ void k_block_min(const int* __restrict__ Dk, int64_t rows, int64_t N, int B, int64_t NB,
+                            int* __restrict__ Bm) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * NB;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / NB, b = t - r * NB;
+    const int* p = Dk + r * N + b * B;
+    const int e = (int)((int64_t)B < N - b * B ? (int64_t)B : N - b * B);
+    int mn = INT_MAX;
+    for (int i = 0; i < e; ++i) mn = min(mn, p[i]);
+    Bm[t] = mn;
+  }
+}
+// per block: the curve values sorted ascending (Cs[b*B ..]) and their
+// exclusive prefix sums (Cp[b*(B+1) ..], B+1 entries)
+constexpr int PRUNE_BMAX = 64;
+__global__ void k_curve_blocks(const double* __restrict__ curve, int64_t N, int B, int64_t NB, double* Cs,
+                               double* Cp) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < NB; b += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)((int64_t)B < N - b * B ? (int64_t)B : N - b * B);
+    double v[PRUNE_BMAX];
+    for (int i = 0; i < e; ++i) {
+      const double x = curve[b * B + i];
+      int j = i;
+      while (j > 0 && v[j - 1] > x) {
+        v[j] = v[j - 1];
+        --j;
+      }
+      v[j] = x;
+    }
+    double acc = 0.0;
+    Cp[b * (B + 1)] = 0.0;
+    for (int i = 0; i < e; ++i) {
+      Cs[b * B + i] = v[i];
+      acc += v[i];
+      Cp[b * (B + 1) + i + 1] = acc;
+    }
+  }
+}
+// LB[s] (taken rows: +inf).  These sums round differently from k_areas', so
+// the bound is lowered by 1e-7 relative: an fp64 sum of N non-negative terms
+// is within (N-1) * 2^-53 relative of its exact value (1.1e-9 at C4's N = 1e7),
+// which covers both sums for N up to ~4e8.
+__global__ void __launch_bounds__(256) k_lb(const int* __restrict__ Bm, int64_t NB, int B, int64_t N,
+                                            const double* __restrict__ Cs, const double* __restrict__ Cp,
+                                            const uint8_t* __restrict__ taken, float twolf, int K15, double dclip,
+                                            double* LB) {
+  __shared__ double sh[8];
+  const int64_t s = blockIdx.x;
+  if (taken[s]) {
+    if (threadIdx.x == 0) LB[s] = PST_INF;
+    return;
+  }
+  double acc = 0.0;
+  for (int64_t b = threadIdx.x; b < NB; b += 256) {
+    double lo, hi;
+    kb_fast(Bm[s * NB + b], twolf, K15, dclip, lo, hi);
+    const int e = (int)((int64_t)B < N - b * B ? (int64_t)B : N - b * B);
+    const double* cs = Cs + b * B;
+    int a = 0, z = e;  // #(curve values < lo)
+    while (a < z) {
+      const int mid = (a + z) >> 1;
+      if (cs[mid] < lo) a = mid + 1;
+      else z = mid;
+    }
+    acc += Cp[b * (B + 1) + a] + (double)(e - a) * lo;
+  }
+  const double t = block_sum<256>(acc, sh);
+  if (threadIdx.x == 0) LB[s] = t * (1.0 - 1e-7);
+}
+__global__ void k_set_bounds(const double* __restrict__ LB, int64_t S, double* alo, double* ahi) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S; s += (int64_t)gridDim.x * blockDim.x) {
+    alo[s] = LB[s];
+    ahi[s] = PST_INF;
   }
 }
 
@@ -830,7 +915,7 @@ int pst_destroy(pst_ctx* c) {
   pst_comm_destroy(c);
   void* ptrs[] = {c->x, c->csum, c->csq, c->chg, c->L.mu, c->L.var, c->L.sd, c->L.nrm, c->L.bias,
                   c->L.cbias, c->L.df, c->L.dg, c->L.mc, c->scratch, c->D, c->work, c->dbg, c->Dk, c->cert,
-                  c->L.hash, c->aux};
+                  c->L.hash, c->aux, c->prune};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->st2) {
@@ -1103,8 +1188,17 @@ static bool use_keys(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
   return have > reserve && (size_t)S * N * sizeof(int) <= have - reserve;
 }
 
+struct PruneBufs {
+  int* Bm = nullptr;  // [S][NB] per-block minimum keys
+  double *Cs = nullptr, *Cp = nullptr, *LB = nullptr;
+  int64_t* segl = nullptr;  // [S] segments to recompute
+  int B = 0;
+  int64_t NB = 0;
+};
 static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N,
-                                    int64_t n, int64_t K, int64_t chunk, pst_snippets* res);
+                                    int64_t n, int64_t K, int64_t chunk, const PruneBufs& pb, pst_snippets* res);
+static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& pb);
+static void prune_free(pst_ctx* c);
 
 // Streamed key path: the key matrix does not fit (or PASTILA_STREAM_KEYS forces it).
 static bool use_keys_streamed(pst_ctx* c, int64_t S, int64_t N, int64_t w) {
@@ -1148,9 +1242,14 @@ int pst_select_snippets(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t K, 
       c->D = nullptr;
       c->D_bytes = 0;
     }
-    const char* sk = getenv("PASTILA_STREAM_KEYS");
-    const int64_t chunk = sk ? std::max<int64_t>(1, atoll(sk)) : key_chunk_rows(c, S, N, m - l + 1);
-    const int r = run_select_keys_streamed(c, m, l, k, S, N, n, K, chunk, res);
+    PruneBufs pb;  // block minima first: the key chunk is sized from what is left
+    int r = prune_alloc(c, S, N, K, pb);
+    if (r == PST_OK) {
+      const char* sk = getenv("PASTILA_STREAM_KEYS");
+      const int64_t chunk = sk ? std::max<int64_t>(1, atoll(sk)) : key_chunk_rows(c, S, N, m - l + 1);
+      r = run_select_keys_streamed(c, m, l, k, S, N, n, K, chunk, pb, res);
+    }
+    prune_free(c);
     if (r != 1) return r;
     c->cert_stats[6]++;  // a certification cap was exceeded: recompute this length exactly
   } else if (use_keys(c, S, N, m - l + 1)) {
@@ -1744,8 +1843,125 @@ static int greedy_step_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t
 // accumulates the per-window attribution state and maxima; pass 1 collects the
 // candidate (segment, window) pairs of the windows pass 0 left uncertain and
 // of profile_max.  Certification and exact resolution as run_select_keys.
+// Block minima for the pruned greedy passes (only when a pass >= 2 exists):
+// the smallest block (16, 32 or 64 windows) whose S x NB keys take at most a
+// third of the device memory left for this length.  PASTILA_PRUNE=0 disables.
+static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& pb) {
+  pb = PruneBufs();
+  if (K < 3) return PST_OK;
+  if (const char* e = getenv("PASTILA_PRUNE"))
+    if (atoi(e) == 0) return PST_OK;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return PST_OK;
+  const size_t have = fr + c->Dk_bytes + c->prune_bytes;
+  for (int B : {16, 32, 64}) {
+    const int64_t NB = (N + B - 1) / B;
+    const size_t need = (size_t)S * NB * 4 + (size_t)NB * (2 * B + 1) * 8 + (size_t)S * 16 + 4096;
+    if (need > have / 3) continue;
+    if (c->Dk) {  // the chunk buffer is sized after this allocation
+      cudaFree(c->Dk);
+      c->Dk = nullptr;
+      c->Dk_bytes = 0;
+    }
+    PST_TRY(pst_ensure(&c->prune, &c->prune_bytes, need));
+    char* p = (char*)c->prune;
+    pb.B = B;
+    pb.NB = NB;
+    pb.Bm = (int*)p;
+    size_t o = ((size_t)S * NB * 4 + 255) & ~(size_t)255;
+    pb.Cs = (double*)(p + o);
+    o += ((size_t)NB * B * 8 + 255) & ~(size_t)255;
+    pb.Cp = (double*)(p + o);
+    o += ((size_t)NB * (B + 1) * 8 + 255) & ~(size_t)255;
+    pb.LB = (double*)(p + o);
+    o += ((size_t)S * 8 + 255) & ~(size_t)255;
+    pb.segl = (int64_t*)(p + o);
+    return PST_OK;
+  }
+  return PST_OK;
+}
+static void prune_free(pst_ctx* c) {
+  if (c->prune) cudaFree(c->prune);
+  c->prune = nullptr;
+  c->prune_bytes = 0;
+}
+// Key-bucket area bounds (k_areas_kb with the current curve) of the listed
+// segments: their key rows are recomputed from a device list, up to `chunk`
+// rows per profile launch (so the row loop and the selection of consecutive
+// batches still overlap).
+static int rows_bounds(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t N, int64_t chunk,
+                       const std::vector<int64_t>& segs, const PruneBufs& pb, const SelBufs& b, const CertBufs& cb,
+                       float twolf, int K15, double dclip) {
+  if (segs.empty()) return PST_OK;
+  PST_CUDA(cudaMemcpyAsync(pb.segl, segs.data(), segs.size() * 8, cudaMemcpyHostToDevice, c->st));
+  for (size_t i = 0; i < segs.size(); i += (size_t)chunk) {
+    const int64_t cnt = std::min<int64_t>(chunk, (int64_t)(segs.size() - i));
+    PST_TRY(launch_mpdist_keys_list(c, m, l, k, pb.segl + i, cnt, c->Dk, N));
+    k_areas_kb<<<(unsigned)cnt, 256, 0, c->st>>>(c->Dk, N, N, b.curve, b.taken, twolf, K15, dclip, cb.alo, cb.ahi,
+                                                 pb.segl + i);
+    c->launches++;
+    PST_CUDA(cudaGetLastError());
+  }
+  PST_CUDA(cudaStreamSynchronize(c->st));  // the host list is reused by the caller
+  return PST_OK;
+}
+// Greedy area bounds of a pass >= 2 without recomputing every row.  Every
+// segment gets alo = LB (a rigorous lower bound), ahi = +inf; the PROBES
+// segments with the smallest LB get their key-bucket bounds, whose smallest
+// upper bound U bounds the winner's exact area from above; every segment with
+// LB <= U is recomputed (the winner, and every segment tied with it, has
+// LB <= area* <= U).  k_greedy_cands then sees exactly the candidates the full
+// pass would give it, or a superset: the exact areas decide as before.
+// done = false: too many candidates, the caller runs the full pass.
+static int pruned_bounds(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t chunk,
+                         const PruneBufs& pb, const SelBufs& b, const CertBufs& cb, float twolf, int K15,
+                         double dclip, bool& done) {
+  constexpr int PROBES = 32;
+  done = false;
+  k_curve_blocks<<<grid_for(pb.NB, 128), 128, 0, c->st>>>(b.curve, N, pb.B, pb.NB, pb.Cs, pb.Cp);
+  k_lb<<<(unsigned)S, 256, 0, c->st>>>(pb.Bm, pb.NB, pb.B, N, pb.Cs, pb.Cp, b.taken, twolf, K15, dclip, pb.LB);
+  k_set_bounds<<<grid_for(S, 256), 256, 0, c->st>>>(pb.LB, S, cb.alo, cb.ahi);
+  c->launches += 3;
+  PST_CUDA(cudaGetLastError());
+  std::vector<double> lb(S);
+  PST_CUDA(cudaMemcpyAsync(lb.data(), pb.LB, (size_t)S * 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  std::vector<int64_t> order;
+  order.reserve(S);
+  for (int64_t s = 0; s < S; ++s)
+    if (lb[s] < HUGE_VAL) order.push_back(s);
+  if (order.empty()) return PST_OK;  // nothing available: the full pass reports it
+  const size_t np = std::min<size_t>(PROBES, order.size());
+  std::partial_sort(order.begin(), order.begin() + np, order.end(),
+                    [&](int64_t a, int64_t z) { return lb[a] < lb[z] || (lb[a] == lb[z] && a < z); });
+  std::vector<int64_t> probes(order.begin(), order.begin() + np);
+  std::sort(probes.begin(), probes.end());
+  PST_TRY(rows_bounds(c, m, l, k, N, chunk, probes, pb, b, cb, twolf, K15, dclip));
+  std::vector<double> hi(np);
+  for (size_t i = 0; i < np; ++i)
+    PST_CUDA(cudaMemcpyAsync(&hi[i], cb.ahi + probes[i], 8, cudaMemcpyDeviceToHost, c->st));
+  PST_CUDA(cudaStreamSynchronize(c->st));
+  const double U = *std::min_element(hi.begin(), hi.end());
+  std::vector<int64_t> rest;
+  for (int64_t s = 0; s < S; ++s)
+    if (lb[s] <= U && !std::binary_search(probes.begin(), probes.end(), s)) rest.push_back(s);
+  if ((int64_t)(rest.size() + np) > S / 2) {  // a full pass is as cheap
+    c->prune_stats[2]++;
+    c->prune_stats[3] += S;
+    return PST_OK;
+  }
+  PST_TRY(rows_bounds(c, m, l, k, N, chunk, rest, pb, b, cb, twolf, K15, dclip));
+  c->prune_stats[0]++;
+  c->prune_stats[1] += (int64_t)(rest.size() + np);
+  if (getenv("PASTILA_DEBUG"))
+    fprintf(stderr, "[pastila] pruned greedy pass: B=%d, %zu of %lld rows recomputed (U=%.17g)\n", pb.B,
+            rest.size() + np, (long long)S, U);
+  done = true;
+  return PST_OK;
+}
+
 static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t n,
-                                    int64_t K, int64_t chunk, pst_snippets* res) {
+                                    int64_t K, int64_t chunk, const PruneBufs& pb, pst_snippets* res) {
   const double twol = 2.0 * (double)l;
   const float twolf = (float)twol;
   int K15;
@@ -1775,9 +1991,16 @@ static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k,
     const bool greedy = pass < K;
     const double* cur = pass == 0 ? nullptr : b.curve;
     if (pass == 1) PST_CUDA(cudaMemsetAsync(cb.cnt + 1, 0, 12, c->st));  // pair counters [1] and [3]
-    for (int64_t s0 = 0; s0 < S; s0 += chunk) {
+    bool pruned = false;  // passes >= 2 only feed greedy areas: recompute just the rows that can win
+    if (pass >= 2 && pb.Bm) PST_TRY(pruned_bounds(c, m, l, k, S, N, chunk, pb, b, cb, twolf, K15, dclip, pruned));
+    for (int64_t s0 = 0; s0 < S && !pruned; s0 += chunk) {
       const int64_t rows = std::min(chunk, S - s0);
       PST_TRY(launch_mpdist_keys(c, m, l, k, s0, s0 + rows, c->Dk, N));
+      if (pass == 0 && pb.Bm) {
+        k_block_min<<<grid_for(rows * pb.NB, 256), 256, 0, c->st>>>(c->Dk, rows, N, pb.B, pb.NB,
+                                                                   pb.Bm + s0 * pb.NB);
+        c->launches++;
+      }
       if (greedy) {
         k_areas_kb<<<(unsigned)rows, 256, 0, c->st>>>(c->Dk, N, N, cur, b.taken + s0, twolf, K15, dclip,
                                                        cb.alo + s0, cb.ahi + s0);
@@ -1925,6 +2148,16 @@ int pst_labels(pst_ctx* c, const double* P, int64_t K, int64_t N, int64_t n, int
   PST_CUDA(cudaGetLastError());
   PST_CUDA(cudaMemcpyAsync(labels, dl, (size_t)n * 8, cudaMemcpyDeviceToHost, c->st));
   PST_CUDA(cudaStreamSynchronize(c->st));
+  return PST_OK;
+}
+
+// Pruned-pass counters of the streamed key path (see pst_ctx::prune_stats).
+int pst_prune_stats(pst_ctx* c, int64_t* out, int reset) {
+  if (!valid(c)) return PST_EINVAL;
+  if (out)
+    for (int i = 0; i < 4; ++i) out[i] = c->prune_stats[i];
+  if (reset)
+    for (int i = 0; i < 4; ++i) c->prune_stats[i] = 0;
   return PST_OK;
 }
 

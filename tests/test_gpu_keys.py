@@ -206,3 +206,44 @@ def test_streamed_key_path_equals_exact_path(monkeypatch, case, chunk):
     assert st[0] == 1
     if case == "planted":
         assert st[6] == 0
+
+
+def _prune_stats(reset=False):
+    out = np.zeros(4, dtype=np.int64)
+    _native.context().call("pst_prune_stats", _native.ptr(out, C.c_int64), 1 if reset else 0)
+    return out
+
+
+@pytest.mark.parametrize("chunk", ["1", "16"])
+@pytest.mark.parametrize("case", ["planted", "random_walk", "two_regime_exact"])
+def test_pruned_greedy_passes_equal_exact_path(monkeypatch, case, chunk):
+    """Streamed key path with K = 5: greedy passes 2..4 recompute only the rows
+    whose block-minimum area bound can still win (or fall back to a full pass);
+    the result == the exact path, field by field, and == the unpruned run."""
+    n = 40_000
+    if case == "planted":
+        x, _ = planted_walk(n, m_act=120, A=3, seed=11)
+    elif case == "random_walk":
+        x = np.cumsum(np.random.default_rng(12).standard_normal(n))
+    else:
+        x, _ = two_regime_series(n, period=32, block_len=64, noise=0.0)
+    s = P.TimeSeries(x)
+    m, K = 128, 5
+    b = _run(s, m, K, exact=True)
+    monkeypatch.setenv("PASTILA_STREAM_KEYS", chunk)
+    _prune_stats(reset=True)
+    _stats(reset=True)
+    a = _run(s, m, K, exact=False)
+    ps, st = _prune_stats(), _stats()
+    _same(a, b)
+    S = n // m
+    if st[6] == 0:  # no certification cap exceeded (exact ties everywhere can exceed one)
+        assert ps[0] + ps[2] == K - 2  # every pass >= 2 was pruned or fell back to a full pass
+    if case != "two_regime_exact":
+        assert st[6] == 0 and ps[0] == K - 2 and ps[1] < (K - 2) * S // 4
+    print(case, chunk, "pruned passes", int(ps[0]), "rows", int(ps[1]), "of", (K - 2) * S, "fallbacks", int(ps[2]))
+    monkeypatch.setenv("PASTILA_PRUNE", "0")
+    _prune_stats(reset=True)
+    c = _run(s, m, K, exact=False)
+    assert _prune_stats()[0] == 0
+    _same(a, c)

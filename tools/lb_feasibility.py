@@ -2,7 +2,7 @@
 C3 series, one length: step-1 areas sum_j min(curve_j, d(s, j)) vs the lower
 bound sum_j min(curve_j, min_{j' in block(j)} d(s, j')); prints how many
 segments the bound cannot exclude, per block size.
-usage: python tools/lb_feasibility.py m"""
+usage: python tools/lb_feasibility.py m [n] [A]   (default: the C3 series, n = 1e6, A = 4)"""
 import ctypes as C, os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -10,7 +10,9 @@ import paper_2401_13680_b200 as P
 from paper_2401_13680_b200 import _native
 from paper_2401_13680_b200.datagen import planted_walk
 m = int(sys.argv[1])
-x, _ = planted_walk(1_000_000, m_act=256, A=4, seed=0)
+n_ = int(float(sys.argv[2])) if len(sys.argv) > 2 else 1_000_000
+A_ = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+x, _ = planted_walk(n_, m_act=256, A=A_, seed=0)
 pr = P.MPdistParams(m)
 l = pr.window_size
 N = x.size - m + 1
@@ -49,9 +51,29 @@ with ctx.using(x):
     area = torch.cat(area)
     area[best] = float("inf")
     amin = float(area.min())
-    res = {"m": m, "S": S, "best0": best, "amin1": amin}
+    res = {"m": m, "S": S, "step": 1, "best0": best, "amin1": amin}
     for B in BS:
         v = torch.cat(lb[B]); v[best] = float("inf")
         res[f"cand_B{B}"] = int((v <= amin).sum())
         res[f"lb_gap_B{B}"] = float(((area - v) / area)[torch.isfinite(area)].mean())
-    print(json.dumps(res))
+    print(json.dumps(res), flush=True)
+    # step 2: curve = min(curve, profile of the step-1 winner)
+    best1 = int(area.argmin())
+    _, d1 = next((s0, d) for s0, d in chunks() if s0 <= best1 < s0 + CH)
+    curve = torch.minimum(curve, d1[best1 % CH])
+    area, lb = [], {B: [] for B in BS}
+    for s0, d in chunks():
+        area.append(torch.minimum(d, curve).sum(1).cpu())
+        for B in BS:
+            nb = (N + B - 1) // B
+            pad = torch.nn.functional.pad(d, (0, nb * B - N), value=float("inf"))
+            bm = pad.view(d.shape[0], nb, B).amin(2)
+            lb[B].append(torch.minimum(bm.repeat_interleave(B, 1)[:, :N], curve).sum(1).cpu())
+    area = torch.cat(area)
+    area[[best, best1]] = float("inf")
+    amin = float(area.min())
+    res = {"m": m, "S": S, "step": 2, "best1": best1, "amin2": amin}
+    for B in BS:
+        v = torch.cat(lb[B]); v[[best, best1]] = float("inf")
+        res[f"cand_B{B}"] = int((v <= amin).sum())
+    print(json.dumps(res), flush=True)

@@ -465,7 +465,24 @@ __device__ __forceinline__ void kb_exact(int K, double twol, double& lo, double&
   lo = e2d(hilo2d(K, 0u), twol);
   hi = e2d(hilo2d(K, 0xffffffffu), twol);
 }
-constexpr int KEY_TWO = 0x40000000;  // key of e = 2.0 (rho clip): f is constant from here on
+constexpr int KEY_TWO = 0x40000000;
+constexpr int NEAR_M = 8;  // nearest (key, segment) pairs kept per window on the streamed path  // key of e = 2.0 (rho clip): f is constant from here on
+// largest key whose interval can reach below hi(K1): every segment whose key at
+// the window is above it is certified farther than the best one
+__device__ int near_kthr(int K1, double twol, int K15) {
+  double l1, h1, lo, hi;
+  kb_exact(K1, twol, l1, h1);
+  if (h1 == 0.0) return K15;         // d* = 0 <=> key < K15, and lo(K15) = 0
+  if (K1 >= KEY_TWO) return INT_MAX;  // f is constant from the clip on
+  int kthr = K1;                      // adjacent buckets differ by ~2^-21 relative in d: a step or two
+  for (;;) {
+    kb_exact(kthr + 1, twol, lo, hi);
+    if (lo > h1) return kthr;
+    if (kthr + 1 >= KEY_TWO) return INT_MAX;
+    ++kthr;
+  }
+}
+
 // Cheap outer bounds in fp32 for the greedy area sums: the bucket edges lo(K)
 // and lo(K+1) >= hi(K) are exact floats for 2^-126 <= e <= 2; fp32 product and
 // sqrt errors (<= 3 ulp = 2^-22.4) are covered by the 2^-20 margins.
@@ -526,16 +543,60 @@ __global__ void __launch_bounds__(256) k_areas_kb(const int* __restrict__ Dk, in
 //   LB[s] = sum_b sum_{j in b} min(curve_j, lo(Bm[s][b])) <= area*[s]
 // (lo = kb_fast's lower bound, monotone in the key), and only the segments
 // with LB[s] <= (an exact upper bound of the winner's area) are recomputed.
+// (also the maximum key of every row, Rx: profile_max candidates)
 __global__ void k_block_min(const int* __restrict__ Dk, int64_t rows, int64_t N, int B, int64_t NB,
-                            int* __restrict__ Bm) {
+                            int* __restrict__ Bm, int* __restrict__ Rx) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * NB;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / NB, b = t - r * NB;
     const int* p = Dk + r * N + b * B;
     const int e = (int)((int64_t)B < N - b * B ? (int64_t)B : N - b * B);
-    int mn = INT_MAX;
-    for (int i = 0; i < e; ++i) mn = min(mn, p[i]);
+    int mn = INT_MAX, mx = INT_MIN;
+    for (int i = 0; i < e; ++i) {
+      mn = min(mn, p[i]);
+      mx = max(mx, p[i]);
+    }
     Bm[t] = mn;
+    atomicMax(Rx + r, mx);
+  }
+}
+__global__ void k_fill_i32(int* p, int v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+// Pass-1 candidate pairs without the key rows: a superset of k_pairs' lists.
+// Attribution (mode 0): k_pairs' exact list when the window's near list
+// (k_near_keys_acc) is complete, else key(s, j) >= Bm[s][j / B], so Bm > kthr
+// excludes s.
+// Maximum (mode 1): key(s, j) <= Rx[s], so Rx < thr excludes s.
+__global__ void k_pairs_sum(const int* __restrict__ Bm, const int* __restrict__ Rx, int64_t S, int64_t NB, int B,
+                            const int* __restrict__ TK, const int32_t* __restrict__ TS, int64_t Nw,
+                            const int64_t* __restrict__ wins, int nwin, const int* __restrict__ K1w, int thr,
+                            int mode, double twol, int K15, int cap, int64_t* pseg, int64_t* pwin, int* cnt) {
+  const int lane = threadIdx.x & 31;
+  const int wv = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (wv >= nwin) return;
+  const int64_t j = wins[wv];
+  const int kthr = mode == 0 ? near_kthr(K1w[j], twol, K15) : thr;
+  if (mode == 0 && TK[(NEAR_M - 1) * Nw + j] > kthr) {  // the near list holds every key <= kthr: exact pairs
+    if (lane < NEAR_M && TK[lane * Nw + j] <= kthr) {
+      const int i = atomicAdd(cnt, 1);
+      if (i < cap) {
+        pseg[i] = TS[lane * Nw + j];
+        pwin[i] = j;
+      }
+    }
+    return;
+  }
+  const int64_t b = j / B;
+  for (int64_t s = lane; s < S; s += 32) {
+    if (mode == 0 ? Bm[s * NB + b] <= kthr : Rx[s] >= kthr) {
+      const int i = atomicAdd(cnt, 1);
+      if (i < cap) {
+        pseg[i] = s;
+        pwin[i] = j;
+      }
+    }
   }
 }
 // per block: the curve values sorted ascending (Cs[b*B ..]) and their
@@ -663,11 +724,21 @@ __global__ void k_near_keys(const int* __restrict__ Dk, int64_t S, int64_t N, in
 // k_near_keys over chunks of segment rows [base, base+rows) arriving in order
 // (streamed key path): running smallest key, first segment, multiplicity,
 // next key and max key per window; finalize with k_near_finalize.
+// (streamed path) Also the NEAR_M smallest (key, segment) pairs of every
+// window, TK/TS [NEAR_M][N], ascending, ties in segment order: pass 1 takes an
+// uncertain window's candidate pairs from them when the list is complete.
 __global__ void k_near_keys_acc(const int* __restrict__ Dk, int64_t rows, int64_t N, int64_t ld, int64_t base,
-                                int first, int* K1w, int32_t* s1w, int* n1w, int* K2w, int* kmaxw) {
+                                int first, int* K1w, int32_t* s1w, int* n1w, int* K2w, int* kmaxw, int* TK,
+                                int32_t* TS) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
     int K1 = INT_MAX, K2 = INT_MAX, KM = INT_MIN, n1 = 0;
     int64_t s1 = 0;
+    int tk[NEAR_M], ts[NEAR_M];
+#pragma unroll
+    for (int i = 0; i < NEAR_M; ++i) {
+      tk[i] = first ? INT_MAX : TK[i * N + j];
+      ts[i] = first ? -1 : TS[i * N + j];
+    }
     if (!first) {
       K1 = K1w[j];
       K2 = K2w[j];
@@ -688,12 +759,35 @@ __global__ void k_near_keys_acc(const int* __restrict__ Dk, int64_t rows, int64_
       } else {
         K2 = min(K2, K);
       }
+      if (K < tk[NEAR_M - 1]) {  // stable insert: after the equal keys already held
+        int pos = NEAR_M - 1;
+#pragma unroll
+        for (int i = NEAR_M - 2; i >= 0; --i)
+          if (tk[i] > K) pos = i;
+#pragma unroll
+        for (int i = NEAR_M - 1; i > 0; --i)
+          if (i > pos) {
+            tk[i] = tk[i - 1];
+            ts[i] = ts[i - 1];
+          }
+#pragma unroll
+        for (int i = 0; i < NEAR_M; ++i)
+          if (i == pos) {
+            tk[i] = K;
+            ts[i] = (int)(base + r);
+          }
+      }
     }
     K1w[j] = K1;
     K2w[j] = K2;
     kmaxw[j] = KM;
     n1w[j] = n1;
     s1w[j] = (int32_t)s1;
+#pragma unroll
+    for (int i = 0; i < NEAR_M; ++i) {
+      TK[i * N + j] = tk[i];
+      TS[i * N + j] = ts[i];
+    }
   }
 }
 __global__ void k_near_finalize(int64_t N, double twol, const int* __restrict__ K1w, const int32_t* __restrict__ s1w,
@@ -742,28 +836,7 @@ __global__ void k_pairs(const int* __restrict__ Dk, int64_t S, int64_t ld, int64
   const int wv = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (wv >= nwin) return;
   const int64_t j = wins[wv];
-  int kthr = thr;
-  if (mode == 0) {  // largest key whose interval can reach below hi(K1)
-    double l1, h1, lo, hi;
-    const int K1 = K1w[j];
-    kb_exact(K1, twol, l1, h1);
-    if (h1 == 0.0) {
-      kthr = K15;  // d* = 0 <=> key < K15, and lo(K15) = 0
-    } else if (K1 >= KEY_TWO) {
-      kthr = INT_MAX;  // f is constant from the clip on
-    } else {
-      kthr = K1;  // adjacent buckets differ by ~2^-21 relative in d: a step or two
-      for (;;) {
-        kb_exact(kthr + 1, twol, lo, hi);
-        if (lo > h1) break;
-        if (kthr + 1 >= KEY_TWO) {
-          kthr = INT_MAX;
-          break;
-        }
-        ++kthr;
-      }
-    }
-  }
+  const int kthr = mode == 0 ? near_kthr(K1w[j], twol, K15) : thr;
   for (int64_t s = lane; s < S; s += 32) {
     const int K = Dk[s * ld + j];
     if (mode == 0 ? K <= kthr : K >= kthr) {
@@ -1192,6 +1265,7 @@ struct PruneBufs {
   int* Bm = nullptr;  // [S][NB] per-block minimum keys
   double *Cs = nullptr, *Cp = nullptr, *LB = nullptr;
   int64_t* segl = nullptr;  // [S] segments to recompute
+  int* Rx = nullptr;        // [S] maximum key of every row
   int B = 0;
   int64_t NB = 0;
 };
@@ -1547,6 +1621,8 @@ struct CertBufs {
   int *cnt, *kmaxw, *K1w, *n1w, *K2w;
   int32_t* s1w;
   uint8_t* unc;
+  int* TK;  // [NEAR_M][N] streamed path: smallest keys per window
+  int32_t* TS;
 };
 static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
   size_t off = 0;
@@ -1560,7 +1636,8 @@ static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
                o_w = take((size_t)CAP_W * 8), o_ps = take((size_t)CAP_P * 8), o_pw = take((size_t)CAP_P * 8),
                o_cnt = take(4 * 4), o_km = take(N * 4), o_k1 = take(N * 4), o_unc = take(N),
                o_mw = take((size_t)CAP_W * 8), o_ps2 = take((size_t)CAP_P * 8), o_pw2 = take((size_t)CAP_P * 8),
-               o_pv2 = take((size_t)CAP_P * 8), o_s1 = take(N * 4), o_n1 = take(N * 4), o_k2 = take(N * 4);
+               o_pv2 = take((size_t)CAP_P * 8), o_s1 = take(N * 4), o_n1 = take(N * 4), o_k2 = take(N * 4),
+               o_tk = take((size_t)NEAR_M * N * 4), o_ts = take((size_t)NEAR_M * N * 4);
   PST_TRY(pst_ensure(&c->cert, &c->cert_bytes, off));
   char* p = (char*)c->cert;
   b.alo = (double*)(p + o_alo);
@@ -1583,6 +1660,8 @@ static int cert_bufs(pst_ctx* c, int64_t S, int64_t N, CertBufs& b) {
   b.s1w = (int32_t*)(p + o_s1);
   b.n1w = (int*)(p + o_n1);
   b.K2w = (int*)(p + o_k2);
+  b.TK = (int*)(p + o_tk);
+  b.TS = (int32_t*)(p + o_ts);
   return PST_OK;
 }
 
@@ -1843,12 +1922,12 @@ static int greedy_step_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t
 // accumulates the per-window attribution state and maxima; pass 1 collects the
 // candidate (segment, window) pairs of the windows pass 0 left uncertain and
 // of profile_max.  Certification and exact resolution as run_select_keys.
-// Block minima for the pruned greedy passes (only when a pass >= 2 exists):
-// the smallest block (16, 32 or 64 windows) whose S x NB keys take at most a
-// third of the device memory left for this length.  PASTILA_PRUNE=0 disables.
+// Block minima for the pruned passes (1 and later): the smallest block (16, 32
+// or 64 windows) whose S x NB keys take at most a third of the device memory
+// left for this length.  PASTILA_PRUNE=0 disables.
 static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& pb) {
   pb = PruneBufs();
-  if (K < 3) return PST_OK;
+  (void)K;  // max(K, 2) >= 2 passes: pass 1 and later can be pruned
   if (const char* e = getenv("PASTILA_PRUNE"))
     if (atoi(e) == 0) return PST_OK;
   size_t fr = 0, tot = 0;
@@ -1856,7 +1935,7 @@ static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& p
   const size_t have = fr + c->Dk_bytes + c->prune_bytes;
   for (int B : {16, 32, 64}) {
     const int64_t NB = (N + B - 1) / B;
-    const size_t need = (size_t)S * NB * 4 + (size_t)NB * (2 * B + 1) * 8 + (size_t)S * 16 + 4096;
+    const size_t need = (size_t)S * NB * 4 + (size_t)NB * (2 * B + 1) * 8 + (size_t)S * 20 + 4096;
     if (need > have / 3) continue;
     if (c->Dk) {  // the chunk buffer is sized after this allocation
       cudaFree(c->Dk);
@@ -1876,6 +1955,8 @@ static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& p
     pb.LB = (double*)(p + o);
     o += ((size_t)S * 8 + 255) & ~(size_t)255;
     pb.segl = (int64_t*)(p + o);
+    o += ((size_t)S * 8 + 255) & ~(size_t)255;
+    pb.Rx = (int*)(p + o);
     return PST_OK;
   }
   return PST_OK;
@@ -1915,9 +1996,10 @@ static int rows_bounds(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t N, i
 // done = false: too many candidates, the caller runs the full pass.
 static int pruned_bounds(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S, int64_t N, int64_t chunk,
                          const PruneBufs& pb, const SelBufs& b, const CertBufs& cb, float twolf, int K15,
-                         double dclip, bool& done) {
+                         double dclip, bool& done, int64_t& rows) {
   constexpr int PROBES = 32;
   done = false;
+  rows = 0;
   k_curve_blocks<<<grid_for(pb.NB, 128), 128, 0, c->st>>>(b.curve, N, pb.B, pb.NB, pb.Cs, pb.Cp);
   k_lb<<<(unsigned)S, 256, 0, c->st>>>(pb.Bm, pb.NB, pb.B, N, pb.Cs, pb.Cp, b.taken, twolf, K15, dclip, pb.LB);
   k_set_bounds<<<grid_for(S, 256), 256, 0, c->st>>>(pb.LB, S, cb.alo, cb.ahi);
@@ -1945,18 +2027,45 @@ static int pruned_bounds(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t S,
   std::vector<int64_t> rest;
   for (int64_t s = 0; s < S; ++s)
     if (lb[s] <= U && !std::binary_search(probes.begin(), probes.end(), s)) rest.push_back(s);
-  if ((int64_t)(rest.size() + np) > S / 2) {  // a full pass is as cheap
-    c->prune_stats[2]++;
-    c->prune_stats[3] += S;
-    return PST_OK;
-  }
+  rows = (int64_t)np;
+  if ((int64_t)(rest.size() + np) > S / 2) return PST_OK;  // a full pass is as cheap
   PST_TRY(rows_bounds(c, m, l, k, N, chunk, rest, pb, b, cb, twolf, K15, dclip));
-  c->prune_stats[0]++;
-  c->prune_stats[1] += (int64_t)(rest.size() + np);
+  rows += (int64_t)rest.size();
   if (getenv("PASTILA_DEBUG"))
-    fprintf(stderr, "[pastila] pruned greedy pass: B=%d, %zu of %lld rows recomputed (U=%.17g)\n", pb.B,
-            rest.size() + np, (long long)S, U);
+    fprintf(stderr, "[pastila] pruned pass: B=%d, %lld of %lld rows recomputed (U=%.17g)\n", pb.B,
+            (long long)rows, (long long)S, U);
   done = true;
+  return PST_OK;
+}
+// Pass 1's candidate pairs from the block minima / row maxima (k_pairs_sum),
+// instead of from the key rows; ok = false when either list exceeds LIM pairs
+// (the exact evaluation of a long superset costs more than a full pass).
+static int pruned_pairs(pst_ctx* c, int64_t S, int64_t N, const PruneBufs& pb, const CertBufs& cb, int nw,
+                        bool need_max, int nmw, int thr, double twol, int K15, bool& ok) {
+  constexpr int LIM = 32768;
+  ok = false;
+  if (nw > 0) {
+    k_pairs_sum<<<(unsigned)((nw * 32 + 255) / 256), 256, 0, c->st>>>(pb.Bm, pb.Rx, S, pb.NB, pb.B, cb.TK, cb.TS,
+                                                                      N, cb.wins, nw,
+                                                                      cb.K1w, 0, 0, twol, K15, CAP_P, cb.pseg,
+                                                                      cb.pwin, cb.cnt + 1);
+    c->launches++;
+  }
+  if (need_max) {
+    k_pairs_sum<<<(unsigned)((nmw * 32 + 255) / 256), 256, 0, c->st>>>(pb.Bm, pb.Rx, S, pb.NB, pb.B, cb.TK, cb.TS,
+                                                                       N, cb.mwins,
+                                                                       nmw, cb.K1w, thr, 1, twol, K15, CAP_P,
+                                                                       cb.pseg2, cb.pwin2, cb.cnt + 3);
+    c->launches++;
+  }
+  PST_CUDA(cudaGetLastError());
+  int n1 = 0, n3 = 0;
+  PST_TRY(read_cnt(c, cb.cnt + 1, n1));
+  PST_TRY(read_cnt(c, cb.cnt + 3, n3));
+  ok = n1 <= LIM && n3 <= LIM;
+  if (getenv("PASTILA_DEBUG"))
+    fprintf(stderr, "[pastila] pass-1 pairs from block summaries: %d attribution, %d maximum (limit %d)\n", n1, n3,
+            LIM);
   return PST_OK;
 }
 
@@ -1991,14 +2100,36 @@ static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k,
     const bool greedy = pass < K;
     const double* cur = pass == 0 ? nullptr : b.curve;
     if (pass == 1) PST_CUDA(cudaMemsetAsync(cb.cnt + 1, 0, 12, c->st));  // pair counters [1] and [3]
-    bool pruned = false;  // passes >= 2 only feed greedy areas: recompute just the rows that can win
-    if (pass >= 2 && pb.Bm) PST_TRY(pruned_bounds(c, m, l, k, S, N, chunk, pb, b, cb, twolf, K15, dclip, pruned));
+    // passes >= 1: recompute only the rows whose greedy area can still win, and
+    // take pass 1's candidate pairs from the block summaries of pass 0
+    bool pruned = false;
+    if (pass >= 1 && pb.Bm) {
+      bool pairs_ok = true;  // the cheap check first: a failed one costs no recomputed rows
+      if (pass == 1) PST_TRY(pruned_pairs(c, S, N, pb, cb, nw, need_max, nmw, thr, twol, K15, pairs_ok));
+      bool areas_ok = !greedy;
+      int64_t prow = 0;
+      if (greedy && pairs_ok)
+        PST_TRY(pruned_bounds(c, m, l, k, S, N, chunk, pb, b, cb, twolf, K15, dclip, areas_ok, prow));
+      pruned = areas_ok && pairs_ok;
+      if (pruned) {
+        c->prune_stats[0]++;
+        c->prune_stats[1] += prow;
+      } else {
+        c->prune_stats[2]++;
+        c->prune_stats[3] += S;
+        if (pass == 1) PST_CUDA(cudaMemsetAsync(cb.cnt + 1, 0, 12, c->st));  // the full pass collects them again
+      }
+    }
+    if (pass == 0 && pb.Bm) {
+      k_fill_i32<<<grid_for(S, 256), 256, 0, c->st>>>(pb.Rx, INT_MIN, S);
+      c->launches++;
+    }
     for (int64_t s0 = 0; s0 < S && !pruned; s0 += chunk) {
       const int64_t rows = std::min(chunk, S - s0);
       PST_TRY(launch_mpdist_keys(c, m, l, k, s0, s0 + rows, c->Dk, N));
       if (pass == 0 && pb.Bm) {
         k_block_min<<<grid_for(rows * pb.NB, 256), 256, 0, c->st>>>(c->Dk, rows, N, pb.B, pb.NB,
-                                                                   pb.Bm + s0 * pb.NB);
+                                                                   pb.Bm + s0 * pb.NB, pb.Rx + s0);
         c->launches++;
       }
       if (greedy) {
@@ -2008,7 +2139,7 @@ static int run_select_keys_streamed(pst_ctx* c, int64_t m, int64_t l, int64_t k,
       }
       if (pass == 0) {
         k_near_keys_acc<<<grid_for(N, 256), 256, 0, c->st>>>(c->Dk, rows, N, N, s0, s0 == 0 ? 1 : 0, cb.K1w,
-                                                            cb.s1w, cb.n1w, cb.K2w, cb.kmaxw);
+                                                            cb.s1w, cb.n1w, cb.K2w, cb.kmaxw, cb.TK, cb.TS);
         c->launches++;
       }
       if (pass == 1) {

@@ -217,9 +217,10 @@ def _prune_stats(reset=False):
 @pytest.mark.parametrize("chunk", ["1", "16"])
 @pytest.mark.parametrize("case", ["planted", "random_walk", "two_regime_exact"])
 def test_pruned_greedy_passes_equal_exact_path(monkeypatch, case, chunk):
-    """Streamed key path with K = 5: greedy passes 2..4 recompute only the rows
-    whose block-minimum area bound can still win (or fall back to a full pass);
-    the result == the exact path, field by field, and == the unpruned run."""
+    """Streamed key path with K = 5: passes 1..4 recompute only the rows whose
+    block-minimum area bound can still win, pass 1 takes its candidate pairs
+    from the block summaries (or a pass falls back to a full one); the result
+    == the exact path, field by field, and == the unpruned run."""
     n = 40_000
     if case == "planted":
         x, _ = planted_walk(n, m_act=120, A=3, seed=11)
@@ -238,12 +239,43 @@ def test_pruned_greedy_passes_equal_exact_path(monkeypatch, case, chunk):
     _same(a, b)
     S = n // m
     if st[6] == 0:  # no certification cap exceeded (exact ties everywhere can exceed one)
-        assert ps[0] + ps[2] == K - 2  # every pass >= 2 was pruned or fell back to a full pass
+        assert ps[0] + ps[2] == K - 1  # every pass >= 1 was pruned or fell back to a full pass
     if case != "two_regime_exact":
-        assert st[6] == 0 and ps[0] == K - 2 and ps[1] < (K - 2) * S // 4
-    print(case, chunk, "pruned passes", int(ps[0]), "rows", int(ps[1]), "of", (K - 2) * S, "fallbacks", int(ps[2]))
+        assert st[6] == 0 and ps[0] == K - 1 and ps[1] < (K - 1) * S // 4
+    print(case, chunk, "pruned passes", int(ps[0]), "rows", int(ps[1]), "of", (K - 1) * S, "fallbacks", int(ps[2]))
     monkeypatch.setenv("PASTILA_PRUNE", "0")
     _prune_stats(reset=True)
     c = _run(s, m, K, exact=False)
     assert _prune_stats()[0] == 0
     _same(a, c)
+
+
+@pytest.mark.parametrize("K", [1, 2])
+def test_pruned_pass1_small_K(monkeypatch, K):
+    """K = 1 (pass 1 only collects pairs) and K = 2 (pass 1 = last greedy step)."""
+    x, _ = planted_walk(30_000, m_act=120, A=3, seed=13)
+    s = P.TimeSeries(x)
+    b = _run(s, 96, K, exact=True)
+    monkeypatch.setenv("PASTILA_STREAM_KEYS", "8")
+    _prune_stats(reset=True)
+    a = _run(s, 96, K, exact=False)
+    ps = _prune_stats()
+    _same(a, b)
+    assert ps[0] + ps[2] == 1
+
+
+def test_pruned_streamed_c3_length_with_uncertain_windows(monkeypatch):
+    """The C3 series at m = 128 (17 attribution windows the key buckets leave
+    uncertain, profiles/r02_c3_certificate.json): streamed with pruned passes
+    1..3, pass 1's pairs taken from the block summaries == the resident key path."""
+    x, _ = planted_walk(1_000_000, m_act=256, A=4, seed=0)
+    s = P.TimeSeries(x)
+    a = _run(s, 128, 4, exact=False)
+    monkeypatch.setenv("PASTILA_STREAM_KEYS", "3000")
+    _prune_stats(reset=True)
+    _stats(reset=True)
+    b = _run(s, 128, 4, exact=False)
+    ps, st = _prune_stats(), _stats()
+    _same(a, b)
+    assert st[6] == 0 and st[3] > 0  # uncertain windows were resolved through the summary pairs
+    assert ps[0] == 3 and ps[2] == 0

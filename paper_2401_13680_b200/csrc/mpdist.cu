@@ -2243,7 +2243,9 @@ static int launch_mpdist_impl(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64
   // selection of batch b (stream st2) overlaps the row loop of batch b+1 (stream st).
   const size_t ab_cta = (size_t)w * (size_t)Tp * SV;
   const size_t per_cta = ab_cta + (size_t)NCmax * SV;
-  size_t budget = (size_t)6 << 30;
+  // both buffers together: larger batches leave fewer row-loop / selection hand-offs
+  // (C3 lengths: 6 GB -> 20-32 GB measured 3% faster, 48 GB no better; tools/gpu_run45-46.sh)
+  size_t budget = (size_t)24 << 30;
   if (const char* e = getenv("PASTILA_SCRATCH_GB")) budget = (size_t)atoll(e) << 30;  // tuning experiments
   {
     size_t fr = 0, tot = 0;

@@ -723,10 +723,10 @@ __global__ void k_near_keys(const int* __restrict__ Dk, int64_t S, int64_t N, in
 
 // k_near_keys over chunks of segment rows [base, base+rows) arriving in order
 // (streamed key path): running smallest key, first segment, multiplicity,
-// next key and max key per window; finalize with k_near_finalize.
-// (streamed path) Also the NEAR_M smallest (key, segment) pairs of every
-// window, TK/TS [NEAR_M][N], ascending, ties in segment order: pass 1 takes an
-// uncertain window's candidate pairs from them when the list is complete.
+// next key and max key per window; finalize with k_near_finalize.  Also the
+// NEAR_M smallest (key, segment) pairs of every window, TK/TS [NEAR_M][N],
+// ascending, ties in segment order: a pruned pass 1 takes an uncertain
+// window's candidate pairs from them when the list is complete.
 __global__ void k_near_keys_acc(const int* __restrict__ Dk, int64_t rows, int64_t N, int64_t ld, int64_t base,
                                 int first, int* K1w, int32_t* s1w, int* n1w, int* K2w, int* kmaxw, int* TK,
                                 int32_t* TS) {

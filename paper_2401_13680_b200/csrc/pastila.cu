@@ -1925,7 +1925,9 @@ static int greedy_step_keys(pst_ctx* c, int64_t m, int64_t l, int64_t k, int64_t
 // Block minima for the pruned passes (1 and later): the smallest block (16, 32
 // or 64 windows) whose S x NB keys take at most a third of the device memory
 // left for this length.  PASTILA_PRUNE=0 disables.
+static int PRUNE_MEM_PCT = 55;
 static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& pb) {
+  if (const char* e = getenv("PASTILA_PRUNE_MEM_PCT")) PRUNE_MEM_PCT = atoi(e);  // tuning experiments
   pb = PruneBufs();
   (void)K;  // max(K, 2) >= 2 passes: pass 1 and later can be pruned
   if (const char* e = getenv("PASTILA_PRUNE"))
@@ -1936,7 +1938,7 @@ static int prune_alloc(pst_ctx* c, int64_t S, int64_t N, int64_t K, PruneBufs& p
   for (int B : {16, 32, 64}) {
     const int64_t NB = (N + B - 1) / B;
     const size_t need = (size_t)S * NB * 4 + (size_t)NB * (2 * B + 1) * 8 + (size_t)S * 20 + 4096;
-    if (need > have / 3) continue;
+    if (need > have / 100 * PRUNE_MEM_PCT) continue;
     if (c->Dk) {  // the chunk buffer is sized after this allocation
       cudaFree(c->Dk);
       c->Dk = nullptr;
